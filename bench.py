@@ -1,0 +1,463 @@
+#!/usr/bin/env python
+"""Benchmark: fused vs unfused training iterations on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (N=1): configs[1] of BASELINE.json -- MobileNetV2 on synthetic
+CIFAR-10-shaped data (3x32x32, 10 classes), SGD-momentum (lr 0.1, momentum
+0.9, weight decay 5e-4), fp32, batch 128 per GPU, backward-fusion with the
+update on the side stream.  One "step" = one training iteration (forward,
+backward, every parameter updated).  The same iteration is also timed under
+the unfused PyTorch optimizer (torch.optim.SGD, foreach and fused) and under
+our baseline / forward-fusion / inline backward-fusion schedules; the batch
+sweep 32..512 is reported beside the headline.
+
+Prints ONE JSON line (rank 0).  ``value`` = images/s over all ranks with
+inputs resident in HBM, device-timed with CUDA events (max over ranks);
+``e2e`` = the same through the public API with pinned-host inputs copied in
+and the loss read back every step; ``roofline`` = the update kernel's
+achieved algorithmic HBM bandwidth (events around each side-stream launch in
+an instrumented pass) against MEASURED_PEAKS.json; ``cpu_baseline`` = the
+reference's CPU path (oracle port) on the host cores.
+
+``--impl reference`` times the reference's CPU implementation of the path
+(oracle port of optim.py + torch-CPU forward/backward) on the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "train iter time & images/sec (fused vs unfused) at 1/2/4/8 B200; update HBM GB/s"
+UNIT = "images/s"
+WORKLOAD = ("C2: MobileNetV2 (torchvision, 10 classes) on synthetic CIFAR-10 shape 3x32x32, "
+            "SGD-momentum lr 0.1 m 0.9 wd 5e-4, fp32")
+
+
+def parse_args(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--model", default="mobilenet_v2_cifar")
+    ap.add_argument("--batch", type=int, default=128, help="per-GPU batch")
+    ap.add_argument("--schedule", default="backward-fusion",
+                    choices=("baseline", "forward-fusion", "backward-fusion"))
+    ap.add_argument("--workers", type=int, default=2, help="backward-fusion: 1 inline, >1 side stream")
+    ap.add_argument("--grad-reset", default="none", choices=("zero", "none"))
+    ap.add_argument("--sweep", default="32,64,256,512", help="extra per-GPU batches ('' to skip)")
+    ap.add_argument("--no-extras", action="store_true", help="headline only (for profilers)")
+    ap.add_argument("--cpu-iters", type=int, default=2, help="CPU baseline sample iterations")
+    return ap.parse_args(argv)
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+# ---------------------------------------------------------------------------
+
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+
+    def init(self, backend="nccl"):
+        import torch
+        import torch.distributed as dist
+        if self.world > 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            if backend == "nccl":
+                torch.cuda.set_device(self.local)
+            dist.init_process_group(backend, rank=self.rank, world_size=self.world)
+            self.pg = dist.group.WORLD
+        return self
+
+    def barrier(self):
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def max(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+
+class Clocks:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=10)
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for name, v in zip(self.NAMES, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# timing helpers
+# ---------------------------------------------------------------------------
+
+def timed(step, steps: int, warmup: int, dist: Dist, flush=None) -> float:
+    """W warm-up steps, then EXACTLY K steps between barrier+synchronize on both
+    sides, device-timed with CUDA events on the current stream; max over ranks.
+    Returns ms per step."""
+    import torch
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(steps):
+        if flush is not None:
+            flush()
+        step()
+    e1.record(s)
+    torch.cuda.synchronize()
+    dist.barrier()
+    return dist.max(e0.elapsed_time(e1)) / steps
+
+
+def load_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
+                grad_reset=None, opt_impl=None):
+    """Returns (step_fn, graph_or_model, policy_or_opt)."""
+    import torch
+    import torch.nn.functional as F
+
+    import paper_2104_00237_b200 as of
+    from paper_2104_00237_b200.models import synthetic_batch
+
+    x, y = synthetic_batch(args.model, batch, device=device, seed=seed)
+    if opt_impl is not None:  # unfused torch.optim baseline
+        g = of.build_classifier(args.model, device=device, seed=seed)
+        net = g.module
+        for h in g._pre_handles:
+            h.remove()
+        kw = {"foreach": True} if opt_impl == "foreach" else {"fused": True}
+        opt = torch.optim.SGD(net.parameters(), lr=0.1, momentum=0.9, weight_decay=5e-4, **kw)
+
+        def step():
+            opt.zero_grad(set_to_none=True)
+            F.cross_entropy(net(x), y).backward()
+            opt.step()
+        return step, net, opt
+
+    g = of.build_classifier(args.model, device=device, seed=seed)
+    g.track_counts = True
+    pol = of.OptimizerPolicy("sgd-momentum", eta=0.1, alpha=0.9, weight_decay=5e-4,
+                             grad_reset=grad_reset or args.grad_reset)
+    w = args.workers if workers is None else workers
+    if schedule == "baseline":
+        def step():
+            of.run_baseline(g, pol, (x, y), timing=False)
+    elif schedule == "forward-fusion":
+        def step():
+            of.run_forward_fusion(g, pol, (x, y), timing=False)
+    else:
+        def step():
+            of.run_backward_fusion(g, pol, (x, y), workers=w, timing=False)
+    return step, g, pol
+
+
+def measure_update_kernel(args, device, peaks) -> dict:
+    """Standalone roofline of the multi-tensor kernel: one launch over a whole
+    parameter set, L2 flushed before every launch (VGG-16 shapes with Adam --
+    the update-bound config C3 -- and the MobileNetV2 set with SGD-momentum)."""
+    import torch
+
+    import paper_2104_00237_b200 as of
+    from paper_2104_00237_b200.optim import algorithmic_bytes
+
+    out = {}
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=device)
+    for name, model, kind in (("vgg16_adam", "vgg16", "adam"),
+                              ("mobilenet_v2_sgdm", "mobilenet_v2_cifar", "sgd-momentum")):
+        g = of.build_classifier(model, device=device)
+        pol = of.OptimizerPolicy(kind, eta=1e-4)
+        params = g.parameters
+        for p in params:
+            p.value.grad = torch.randn_like(p.value) * 0.01
+        pol.grad_reset = "zero"
+        times = []
+        for i in range(8):
+            pol.begin_iteration()
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            pol.step_params(params)
+            e1.record()
+            torch.cuda.synchronize()
+            if i >= 3:
+                times.append(e0.elapsed_time(e1))
+        nbytes = algorithmic_bytes(kind, params)
+        t = statistics.median(times) / 1e3
+        gbs = nbytes / t / 1e9
+        out[name] = {"bytes": nbytes, "us": t * 1e6, "achieved_gbs": round(gbs, 1),
+                     "frac": round(gbs / peaks["hbm_gbs"], 4), "tensors": len(params),
+                     "launches": (len(params) + 63) // 64}
+        del g, params
+        torch.cuda.empty_cache()
+    return out
+
+
+def measure_in_situ(args, device, peaks, steps: int) -> dict:
+    """Per-launch duration of the backward-fusion update kernel inside real
+    training iterations (events around each side-stream launch)."""
+    import torch
+
+    from paper_2104_00237_b200.optim import algorithmic_bytes
+    step, g, pol = make_runner(args, args.batch, "backward-fusion", device, workers=2)
+    for _ in range(3):
+        step()
+    eng = g._bf_engine
+    eng.profile = []
+    for _ in range(steps):
+        step()
+    torch.cuda.synchronize()
+    recs = eng.profile
+    eng.profile = None
+    tot_ms = sum(a.elapsed_time(b) for a, b, _ in recs)
+    tot_bytes = sum(algorithmic_bytes(pol.kind, ps) for _, _, ps in recs)
+    n = len(recs)
+    gbs = tot_bytes / (tot_ms / 1e3) / 1e9
+    return {"launches_per_step": n // steps, "avg_bytes": tot_bytes / n, "avg_us": tot_ms / n * 1e3,
+            "achieved_gbs": gbs, "frac": gbs / peaks["hbm_gbs"]}
+
+
+def cpu_baseline(args, iters: int) -> dict:
+    from oracle import timing
+    r = timing.cpu_training_sample(args.model, args.batch, iters, "sgd-momentum",
+                                   dict(eta=0.1, alpha=0.9, weight_decay=5e-4))
+    return {"value": round(r["images_per_s"], 3), "unit": UNIT, "cores": r["threads"],
+            "kind": "port",
+            "sample": (f"{iters} iterations at batch {args.batch}: torch-CPU forward/backward on "
+                       f"{r['threads']} threads ({r['fwd_bwd_ms']:.0f} ms) + reference update "
+                       f"(oracle port of optim.py, numpy, 1 thread, {r['update_ms']:.1f} ms "
+                       f"over {r['update_elems']} params)")}
+
+
+def run_ours(args) -> dict:
+    import torch
+
+    from paper_2104_00237_b200 import _native
+    dist = Dist().init("nccl")
+    device = torch.device("cuda", dist.local)
+    torch.cuda.set_device(device)
+    torch.backends.cudnn.benchmark = True
+    peaks = load_peaks()
+    if dist.world > 1:
+        raise SystemExit("multi-GPU data parallel bench: see paper_2104_00237_b200.dp (not wired yet)")
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+    flush = flush_buf.zero_
+
+    step, g, pol = make_runner(args, args.batch, args.schedule, device)
+    n0 = _native.launch_count()
+    with Clocks(dist.local) as clk:
+        ms = timed(step, args.steps, args.warmup, dist, flush)
+    launches = (_native.launch_count() - n0) * args.steps // (args.steps + args.warmup)
+    clocks = clk.summary()
+    value = dist.world * args.batch * 1e3 / ms
+    res = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": dist.world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+           "data": "synthetic (x~N(0,1) [b,3,32,32], y~U{0..9}; random-init weights)",
+           "config": {"workload": WORKLOAD, "model": args.model, "batch_per_gpu": args.batch,
+                      "global_batch": args.batch * dist.world, "schedule": args.schedule,
+                      "workers": args.workers, "grad_reset": args.grad_reset,
+                      "parallelism": f"dp{dist.world}",
+                      "l2": "256 MiB buffer zeroed before every timed step (inside the timed region)"},
+           "gpu_launches": launches}
+    del step, g, pol
+    if not args.no_extras:
+        sched = {}
+        variants = [("torch.optim.SGD(foreach)", "baseline", None, None, "foreach"),
+                    ("torch.optim.SGD(fused)", "baseline", None, None, "fused"),
+                    ("ours:baseline", "baseline", None, None, None),
+                    ("ours:forward-fusion", "forward-fusion", None, None, None),
+                    ("ours:backward-fusion(w=1)", "backward-fusion", 1, None, None),
+                    ("ours:backward-fusion(w=2)", "backward-fusion", 2, None, None),
+                    ("ours:backward-fusion(w=2,zero)", "backward-fusion", 2, "zero", None)]
+        for b in [args.batch] + [int(s) for s in args.sweep.split(",") if s.strip()]:
+            row = {}
+            for name, sch, w, gr, opt in variants:
+                if b != args.batch and name not in ("torch.optim.SGD(foreach)",
+                                                    "ours:forward-fusion",
+                                                    "ours:backward-fusion(w=2)"):
+                    continue
+                st, *_ = make_runner(args, b, sch, device, workers=w, grad_reset=gr, opt_impl=opt)
+                t = timed(st, args.steps, args.warmup, dist, flush)
+                row[name] = {"ms_per_step": round(t, 4), "images_per_s": round(b * 1e3 / t, 1)}
+                del st
+                torch.cuda.empty_cache()
+            base = row["torch.optim.SGD(foreach)"]["ms_per_step"]
+            for k, v in row.items():
+                v["speedup_vs_torch_foreach"] = round(base / v["ms_per_step"], 4)
+            sched[str(b)] = row
+        res["schedules"] = sched
+        res["speedup_vs_unfused_torch"] = sched[str(args.batch)][
+            f"ours:{args.schedule}" + ("(w=%d)" % args.workers if args.schedule == "backward-fusion" else "")
+        ]["speedup_vs_torch_foreach"] if args.schedule == "backward-fusion" else None
+        # end to end through the public API: pinned host batch -> device, loss -> host
+        res["e2e"] = e2e(args, device, dist)
+        ins = measure_in_situ(args, device, peaks, 5)
+        std = measure_update_kernel(args, device, peaks)
+        res["roofline"] = {"bound": "hbm", "kernel": "mt_step_kernel (backward-fusion, side stream)",
+                           "achieved": round(ins["achieved_gbs"], 1), "peak": peaks["hbm_gbs"],
+                           "unit": "GB/s", "frac": round(ins["frac"], 4), "traffic": None,
+                           "peak_source": peaks["source"],
+                           "per_launch": {"avg_bytes": round(ins["avg_bytes"]), "avg_us": round(ins["avg_us"], 3),
+                                          "launches_per_step": ins["launches_per_step"]},
+                           "standalone_single_launch": std}
+        if dist.rank == 0 and dist.world == 1:
+            res["cpu_baseline"] = cpu_baseline(args, args.cpu_iters)
+    res["clocks"] = clocks
+    dist.close()
+    return res
+
+
+def e2e(args, device, dist) -> dict:
+    import torch
+
+    import paper_2104_00237_b200 as of
+    from paper_2104_00237_b200.models import synthetic_batch
+    xh, yh = synthetic_batch(args.model, args.batch, device="cpu")
+    xh, yh = xh.pin_memory(), yh.pin_memory()
+    g = of.build_classifier(args.model, device=device)
+    pol = of.OptimizerPolicy("sgd-momentum", eta=0.1, alpha=0.9, weight_decay=5e-4,
+                             grad_reset=args.grad_reset)
+    run = {"baseline": of.run_baseline, "forward-fusion": of.run_forward_fusion,
+           "backward-fusion": of.run_backward_fusion}[args.schedule]
+    kw = {"workers": args.workers} if args.schedule == "backward-fusion" else {}
+
+    def step():
+        x = xh.to(device, non_blocking=True)
+        y = yh.to(device, non_blocking=True)
+        rep = run(g, pol, (x, y), timing=False, **kw)
+        return rep.loss.item()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    torch.cuda.synchronize()
+    dt = dist.max(time.perf_counter() - t0)
+    return {"value": round(dist.world * args.batch * args.steps / dt, 2), "unit": UNIT,
+            "h2d_bytes_per_step": xh.numel() * xh.element_size() + yh.numel() * yh.element_size(),
+            "d2h_bytes_per_step": 4}
+
+
+# ---------------------------------------------------------------------------
+# reference arm
+# ---------------------------------------------------------------------------
+
+def run_reference(args) -> dict | None:
+    dist = Dist()
+    if dist.rank != 0:
+        return None
+    from oracle import timing
+    kw = dict(eta=0.1, alpha=0.9, weight_decay=5e-4)
+    timing.cpu_training_sample(args.model, args.batch, 1, "sgd-momentum", kw)  # warm-up
+    r = timing.cpu_training_sample(args.model, args.batch, max(args.steps, 1), "sgd-momentum", kw)
+    v = round(r["images_per_s"], 3)
+    return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 0,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(r["ms_per_iter"], 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": {"workload": WORKLOAD, "model": args.model,
+                                             "batch_per_gpu": args.batch, "schedule": "baseline"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": r["threads"], "kind": "port",
+                             "sample": (f"each step: one iteration at batch {args.batch}, "
+                                        f"torch-CPU fwd/bwd on {r['threads']} threads + the "
+                                        f"reference update (numpy oracle port, 1 thread)")},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main(argv=None):
+    args = parse_args(argv)
+    if args.impl == "reference":
+        res = run_reference(args)
+    else:
+        res = run_ours(args)
+    if res is not None and int(os.environ.get("RANK", "0")) == 0:
+        print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,155 @@
+/*
+ * optfuse_b200.h -- C ABI of the B200 (sm_100a) fused-optimizer kernel library.
+ *
+ * This is the drop-in boundary for the hot path of Optimizer Fusion
+ * (arXiv 2104.00237).  The reference (`optfuse`, pure Python/numpy) has no FFI;
+ * its plugin boundary is the Python method
+ *
+ *     OptimizerPolicy.step(param, step_t=None, trace=None)
+ *         /root/reference/pkg/src/optfuse/optim.py:74-115  (contract + axpy)
+ *         /root/reference/pkg/src/optfuse/optim.py:117-148 (_delta per kind)
+ *         /root/reference/pkg/src/optfuse/tensor.py:140-144 (axpy_inplace)
+ *
+ * and the global-information transform
+ *
+ *     clip_by_global_norm(graph, max_norm)
+ *         /root/reference/pkg/src/optfuse/optim.py:151-172
+ *
+ * Every entry point below takes plain device pointers, element counts, host
+ * scalars and a CUDA stream (as `void*`, i.e. a `cudaStream_t`).  No torch
+ * types cross this boundary.  Ownership: the caller owns every buffer; the
+ * library never allocates, frees or synchronises.  Errors are returned as an
+ * `of_status`; invalid arguments are rejected before anything is launched
+ * (mirroring the reference's raise-before-mutate convention), and the
+ * contract errors of the reference (SchedulingContractError,
+ * GlobalInfoRequired, ConfigError) are raised by the host layer above this ABI
+ * before it is called.  Thread-safety: all entry points are reentrant; the
+ * only per-thread state is the last error message.
+ *
+ * Arithmetic contract: for kinds SGD..ADAM every element update performs the
+ * exact IEEE-754 operation sequence of the reference's numpy code (one
+ * correctly rounded f32/f64 operation per numpy operation, source order, no
+ * FMA contraction), so results are bit-identical to the reference on the same
+ * inputs.  Host scalars are passed as doubles exactly as Python holds them and
+ * are rounded to the tensor precision once, as numpy >= 2 (NEP 50) does.
+ */
+#ifndef OPTFUSE_B200_H
+#define OPTFUSE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OF_ABI_VERSION 1
+
+typedef enum of_status {
+  OF_OK = 0,
+  OF_ERR_INVALID = 1,      /* bad argument; nothing was launched */
+  OF_ERR_UNSUPPORTED = 2,  /* dtype/kind/flag combination not built */
+  OF_ERR_CUDA = 3          /* the CUDA runtime rejected a launch */
+} of_status;
+
+typedef enum of_dtype {
+  OF_F32 = 0,
+  OF_F64 = 1,
+  OF_BF16 = 2
+} of_dtype;
+
+/* optim.py:22 KINDS (minus "newton", which has no per-parameter step,
+ * optim.py:82-83) plus AdamW (decoupled decay, torch.optim.AdamW semantics;
+ * not in the reference). */
+typedef enum of_kind {
+  OF_SGD = 0,           /* optim.py:119-120 */
+  OF_SGD_MOMENTUM = 1,  /* optim.py:121-125 */
+  OF_ADAGRAD = 2,       /* optim.py:126-129 */
+  OF_RMSPROP = 3,       /* optim.py:130-133 */
+  OF_ADADELTA = 4,      /* optim.py:134-140 */
+  OF_ADAM = 5,          /* optim.py:141-148 (coupled weight decay) */
+  OF_ADAMW = 6          /* torch.optim.AdamW(foreach=False) formula */
+} of_kind;
+
+/* step flags */
+#define OF_FLAG_ZERO_GRAD 0x1u   /* write grad = 0 after reading it (optim.py:111) */
+#define OF_FLAG_SHADOW_BF16 0x2u /* also write a bf16 copy of the new parameter */
+
+/* Hyper-parameters of one policy step (optim.py:42-51).  Scalars are the
+ * Python doubles; the library rounds them to the tensor precision. */
+typedef struct of_hparams {
+  int32_t kind;            /* of_kind */
+  int32_t reserved;
+  double eta;              /* step size */
+  double alpha;            /* momentum decay */
+  double weight_decay;     /* coupled for SGD..ADAM (optim.py:102-104), decoupled for ADAMW */
+  double epsilon;
+  double beta1;
+  double beta2;
+  double rho;
+  double bias_correction1; /* ADAM/ADAMW: 1 - beta1**t, in double (optim.py:145) */
+  double bias_correction2; /* ADAM/ADAMW: 1 - beta2**t, in double (optim.py:146) */
+} of_hparams;
+
+/* A list of parameters updated by one launch.  Arrays live in HOST memory and
+ * hold DEVICE pointers; they are read during the call only.  History slots
+ * follow optim.py:24-31:
+ *   SGD: none | SGD_MOMENTUM: state0=momentum | ADAGRAD: state0=sum_sq
+ *   RMSPROP: state0=square_avg | ADADELTA: state0=square_avg, state1=acc_delta
+ *   ADAM/ADAMW: state0=exp_avg, state1=exp_avg_sq
+ * param/state dtype: OF_F32 or OF_F64.  grad dtype: same as param, or OF_BF16
+ * with OF_F32 params (bf16 gradients into fp32 master weights). */
+typedef struct of_tensor_list {
+  int32_t n;               /* number of tensors, >= 0 */
+  int32_t param_dtype;     /* of_dtype of param and state slots */
+  int32_t grad_dtype;      /* of_dtype of grad */
+  int32_t reserved;
+  void* const* param;      /* [n] */
+  void* const* grad;       /* [n] */
+  void* const* state0;     /* [n] or NULL when the kind has no slot */
+  void* const* state1;     /* [n] or NULL when the kind has < 2 slots */
+  void* const* shadow;     /* [n] bf16 copies, required with OF_FLAG_SHADOW_BF16 */
+  const int64_t* numel;    /* [n] element counts (0 allowed: skipped) */
+} of_tensor_list;
+
+int of_abi_version(void);
+const char* of_status_string(int status);
+/* Message of the last error returned on this thread ("" if none). */
+const char* of_last_error(void);
+/* Number of kernels this library has launched in this process (all threads). */
+uint64_t of_launch_count(void);
+
+/* One policy step over every tensor of `list` (OptimizerPolicy.step,
+ * optim.py:74-115, applied to several parameters in one multi-tensor launch).
+ * grad_scale_dev: NULL, or a device f32 scalar multiplied into every gradient
+ * before the update (the global-norm clip factor, optim.py:170). */
+int of_policy_step_mt(const of_tensor_list* list, const of_hparams* hp,
+                      const float* grad_scale_dev, uint32_t flags, void* stream);
+
+/* Convenience wrappers with the kind fixed (same semantics). */
+int of_sgdm_mt(const of_tensor_list* list, double eta, double alpha, double weight_decay,
+               const float* grad_scale_dev, uint32_t flags, void* stream);
+int of_adam_mt(const of_tensor_list* list, double eta, double beta1, double beta2,
+               double epsilon, double weight_decay, double bias_correction1,
+               double bias_correction2, int decoupled_weight_decay,
+               const float* grad_scale_dev, uint32_t flags, void* stream);
+
+/* Sum of squares of every grad in `list`, accumulated in f64 with a fixed
+ * (deterministic) reduction order (optim.py:160-164).  Uses `workspace_dev`
+ * (>= of_sqnorm_workspace_len() doubles).  Writes *out_dev = sum, or
+ * *out_dev += sum when accumulate != 0 (stream-ordered, so chained calls over
+ * several lists are deterministic). */
+int64_t of_sqnorm_workspace_len(void);
+int of_sqnorm_mt(const of_tensor_list* list, double* workspace_dev, int64_t workspace_len,
+                 double* out_dev, int accumulate, void* stream);
+
+/* norm = sqrt(*sqnorm_dev); factor = norm <= max_norm ? 1 : max_norm / norm
+ * (optim.py:165-168, in double); *coef_dev = (float)factor (the f32 multiplier
+ * numpy applies at optim.py:170); *factor_dev = factor when non-NULL. */
+int of_clip_coef(const double* sqnorm_dev, double max_norm, float* coef_dev,
+                 double* factor_dev, void* stream);
+
+#ifdef __cplusplus
+}  /* extern "C" */
+#endif
+
+#endif /* OPTFUSE_B200_H */

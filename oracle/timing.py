@@ -1,0 +1,62 @@
+"""CPU baseline leg of bench.py (test/bench infrastructure, never the product).
+
+Times the reference's CPU path for the benchmark workload on the host cores:
+the reference update (optim.py:74-148, restated bit-exactly in
+oracle.optim_ref -- numpy, single-threaded as in the reference) applied to a
+real network's parameters, after a forward/backward pass on torch-CPU.  The
+reference's own autodiff engine (graph.py) only supports its synthetic chains,
+so torch-CPU stands in for it; that stage uses every host core allowed.
+"""
+
+from __future__ import annotations
+
+import os
+import time
+
+import numpy as np
+
+from . import optim_ref
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_training_sample(model_name: str, batch: int, iters: int, kind: str, hp: dict,
+                        threads: int | None = None, seed: int = 0) -> dict:
+    """``iters`` iterations of forward/backward (torch CPU) + the reference
+    update (numpy oracle) on ``model_name``; returns timings and images/s."""
+    import torch
+    import torch.nn.functional as F
+
+    from paper_2104_00237_b200.models import CLASSIFIERS, synthetic_batch
+
+    threads = threads or host_cores()
+    torch.set_num_threads(threads)
+    torch.manual_seed(seed)
+    net = CLASSIFIERS[model_name][0]()
+    x, y = synthetic_batch(model_name, batch, device="cpu", seed=seed)
+    params = [p for p in net.parameters() if p.requires_grad]
+    h = optim_ref.Hyper(kind=kind, **hp)
+    slots = [dict() for _ in params]
+    fb, upd = [], []
+    for t in range(1, iters + 1):
+        t0 = time.perf_counter()
+        loss = F.cross_entropy(net(x), y)
+        loss.backward()
+        t1 = time.perf_counter()
+        for p, sl in zip(reversed(params), reversed(slots)):
+            theta = p.detach().numpy().reshape(-1)   # shares storage with the torch parameter
+            grad = p.grad.numpy().reshape(-1)
+            optim_ref.step(kind, h, theta, grad, sl, t)
+        t2 = time.perf_counter()
+        fb.append(t1 - t0)
+        upd.append(t2 - t1)
+    n_elem = sum(p.numel() for p in params)
+    per_iter = float(np.mean(fb) + np.mean(upd))
+    return {"images_per_s": batch / per_iter, "ms_per_iter": per_iter * 1e3,
+            "fwd_bwd_ms": float(np.mean(fb)) * 1e3, "update_ms": float(np.mean(upd)) * 1e3,
+            "update_elems": n_elem, "threads": threads, "batch": batch, "iters": iters}

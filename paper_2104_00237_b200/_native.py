@@ -1,0 +1,105 @@
+"""ctypes binding of the C ABI in include/optfuse_b200.h (liboptfuse_b200.so).
+
+The product path has exactly one implementation: the sm_100a kernels in
+``csrc/optfuse_kernels.cu``.  If the shared library is missing this module
+raises ``NativeLibraryError`` -- there is no CPU or PyTorch fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+from .errors import NativeLibraryError
+
+LIB_NAME = "liboptfuse_b200.so"
+LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
+
+OF_OK, OF_ERR_INVALID, OF_ERR_UNSUPPORTED, OF_ERR_CUDA = 0, 1, 2, 3
+OF_F32, OF_F64, OF_BF16 = 0, 1, 2
+OF_FLAG_ZERO_GRAD = 0x1
+OF_FLAG_SHADOW_BF16 = 0x2
+
+# of_kind (optim.py:22 minus newton, plus adamw)
+KIND_CODES = {"sgd": 0, "sgd-momentum": 1, "adagrad": 2, "rmsprop": 3, "adadelta": 4,
+              "adam": 5, "adamw": 6}
+
+# every symbol include/optfuse_b200.h declares (checked by tests/test_native_abi.py)
+SYMBOLS = ("of_abi_version", "of_status_string", "of_last_error", "of_launch_count",
+           "of_policy_step_mt", "of_sgdm_mt", "of_adam_mt", "of_sqnorm_workspace_len",
+           "of_sqnorm_mt", "of_clip_coef")
+
+_vp = ctypes.c_void_p
+_PP = ctypes.POINTER(ctypes.c_void_p)
+
+
+class OfHparams(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("eta", ctypes.c_double), ("alpha", ctypes.c_double),
+                ("weight_decay", ctypes.c_double), ("epsilon", ctypes.c_double),
+                ("beta1", ctypes.c_double), ("beta2", ctypes.c_double), ("rho", ctypes.c_double),
+                ("bias_correction1", ctypes.c_double), ("bias_correction2", ctypes.c_double)]
+
+
+class OfTensorList(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("param_dtype", ctypes.c_int32),
+                ("grad_dtype", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("param", _PP), ("grad", _PP), ("state0", _PP), ("state1", _PP),
+                ("shadow", _PP), ("numel", ctypes.POINTER(ctypes.c_int64))]
+
+
+_lib = None
+
+
+def lib():
+    """Load the kernel library once; raise NativeLibraryError if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = Path(os.environ.get("OPTFUSE_B200_LIB", LIB_PATH))
+    if not path.exists():
+        raise NativeLibraryError(
+            f"{path} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(the fused-optimizer path has no CPU fallback)")
+    try:
+        so = ctypes.CDLL(str(path))
+    except OSError as e:
+        raise NativeLibraryError(f"cannot load {path}: {e}") from e
+    so.of_abi_version.restype = ctypes.c_int
+    so.of_status_string.restype = ctypes.c_char_p
+    so.of_status_string.argtypes = [ctypes.c_int]
+    so.of_last_error.restype = ctypes.c_char_p
+    so.of_launch_count.restype = ctypes.c_uint64
+    so.of_policy_step_mt.restype = ctypes.c_int
+    so.of_policy_step_mt.argtypes = [ctypes.POINTER(OfTensorList), ctypes.POINTER(OfHparams),
+                                     _vp, ctypes.c_uint32, _vp]
+    so.of_sgdm_mt.restype = ctypes.c_int
+    so.of_sgdm_mt.argtypes = [ctypes.POINTER(OfTensorList), ctypes.c_double, ctypes.c_double,
+                              ctypes.c_double, _vp, ctypes.c_uint32, _vp]
+    so.of_adam_mt.restype = ctypes.c_int
+    so.of_adam_mt.argtypes = [ctypes.POINTER(OfTensorList)] + [ctypes.c_double] * 7 + [
+        ctypes.c_int, _vp, ctypes.c_uint32, _vp]
+    so.of_sqnorm_workspace_len.restype = ctypes.c_int64
+    so.of_sqnorm_mt.restype = ctypes.c_int
+    so.of_sqnorm_mt.argtypes = [ctypes.POINTER(OfTensorList), _vp, ctypes.c_int64, _vp,
+                                ctypes.c_int, _vp]
+    so.of_clip_coef.restype = ctypes.c_int
+    so.of_clip_coef.argtypes = [_vp, ctypes.c_double, _vp, _vp, _vp]
+    if so.of_abi_version() != 1:
+        raise NativeLibraryError(f"{path}: ABI version {so.of_abi_version()} != 1")
+    _lib = so
+    return so
+
+
+def check(status: int, what: str) -> None:
+    if status != OF_OK:
+        so = lib()
+        msg = so.of_last_error().decode(errors="replace")
+        raise NativeLibraryError(
+            f"{what}: {so.of_status_string(status).decode()} ({msg})")
+
+
+def launch_count() -> int:
+    """Kernels launched by liboptfuse_b200.so in this process."""
+    return int(lib().of_launch_count())

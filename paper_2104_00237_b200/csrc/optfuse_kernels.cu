@@ -1,0 +1,694 @@
+// optfuse_kernels.cu -- sm_100a multi-tensor optimizer-update kernels behind the
+// C ABI declared in include/optfuse_b200.h.
+//
+// What this replaces in the reference (/root/reference/pkg/src/optfuse):
+//   OptimizerPolicy.step   optim.py:74-115   (coupled wd, _delta, grad reset, axpy)
+//   OptimizerPolicy._delta optim.py:117-148  (one functor per kind below)
+//   axpy_inplace           tensor.py:140-144 (theta += 1.0 * delta, fused)
+//   clip_by_global_norm    optim.py:151-172  (sum of squares + factor; the factor
+//                                             is folded into the update as a
+//                                             device scalar, no second grad pass)
+//
+// Design (B200): the update is purely HBM-bound (20-28 algorithmic bytes per
+// element, ~0.5 flop/byte), so the kernel is a grid-stride loop over fixed
+// 4096-element tiles of a list of tensors whose pointers travel in the kernel
+// parameter block (__grid_constant__, no metadata copy).  Each thread moves
+// 128-bit vectors of every stream (theta, grad, history slots), issuing all of
+// its loads for kUnroll vectors before any math so that each SM keeps tens of
+// KB in flight.  The grid is sized to the SM count x resident CTAs.  Arithmetic
+// uses explicit round-to-nearest intrinsics (no FMA contraction) in the exact
+// order numpy evaluates the reference's expressions, so the result is
+// bit-identical to the reference for f32 and f64.
+#include "../../include/optfuse_b200.h"
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kVec = 4;
+constexpr int kUnroll = 4;
+constexpr int kTile = kThreads * kVec * kUnroll;  // elements per tile
+constexpr int kCtasPerSm = 8;
+constexpr int kSqnormWorkspace = 148 * 8 * 4;      // >= any sqnorm grid we launch
+
+std::atomic<uint64_t> g_launches{0};
+thread_local char g_err[512] = "";
+
+int fail(int status, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return status;
+}
+
+int check_launch(const char* what) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(OF_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return OF_OK;
+}
+
+int sm_count() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (cache[dev] == 0) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      n = 148;
+    cache[dev] = n;
+  }
+  return cache[dev];
+}
+
+// ---------------------------------------------------------------------------
+// Correctly rounded scalar ops (one IEEE operation per numpy operation).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float o_add(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float o_sub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float o_mul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float o_div(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ float o_sqrt(float a) { return __fsqrt_rn(a); }
+__device__ __forceinline__ float o_fma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double o_add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double o_sub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double o_mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double o_div(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ double o_sqrt(double a) { return __dsqrt_rn(a); }
+__device__ __forceinline__ double o_fma(double a, double b, double c) { return __fma_rn(a, b, c); }
+
+// ---------------------------------------------------------------------------
+// Update functors.  Each mirrors one branch of OptimizerPolicy._delta plus the
+// shared prologue/epilogue of OptimizerPolicy.step.  Constants are held in the
+// tensor precision T (host rounds the Python double once, NEP 50).
+// ---------------------------------------------------------------------------
+template <class T>
+struct CoupledWd {
+  T wd;
+  bool on;  // optim.py:103 `if self.weight_decay > 0`
+  __device__ __forceinline__ T apply(T g, T p) const {
+    return on ? o_add(g, o_mul(wd, p)) : g;  // g + wd * theta (new temp, optim.py:104)
+  }
+};
+
+template <class T>
+struct SgdOp {  // optim.py:119-120
+  static constexpr int kSlots = 0;
+  CoupledWd<T> wd;
+  T neg_eta;
+  __device__ __forceinline__ void operator()(T& p, T g, T&, T&) const {
+    g = wd.apply(g, p);
+    p = o_add(p, o_mul(neg_eta, g));  // axpy_inplace(theta, 1.0, -eta*g)
+  }
+};
+
+template <class T>
+struct SgdMomentumOp {  // optim.py:121-125
+  static constexpr int kSlots = 1;
+  CoupledWd<T> wd;
+  T neg_eta, alpha;
+  __device__ __forceinline__ void operator()(T& p, T g, T& buf, T&) const {
+    g = wd.apply(g, p);
+    buf = o_mul(buf, alpha);        // buf *= alpha
+    buf = o_add(buf, g);            // buf += g
+    p = o_add(p, o_mul(neg_eta, buf));
+  }
+};
+
+template <class T>
+struct AdagradOp {  // optim.py:126-129
+  static constexpr int kSlots = 1;
+  CoupledWd<T> wd;
+  T neg_eta, eps;
+  __device__ __forceinline__ void operator()(T& p, T g, T& acc, T&) const {
+    g = wd.apply(g, p);
+    acc = o_add(acc, o_mul(g, g));
+    p = o_add(p, o_div(o_mul(neg_eta, g), o_add(o_sqrt(acc), eps)));
+  }
+};
+
+template <class T>
+struct RmspropOp {  // optim.py:130-133
+  static constexpr int kSlots = 1;
+  CoupledWd<T> wd;
+  T neg_eta, eps, rho, one_minus_rho;
+  __device__ __forceinline__ void operator()(T& p, T g, T& sq, T&) const {
+    g = wd.apply(g, p);
+    sq = o_add(o_mul(rho, sq), o_mul(one_minus_rho, o_mul(g, g)));
+    p = o_add(p, o_div(o_mul(neg_eta, g), o_add(o_sqrt(sq), eps)));
+  }
+};
+
+template <class T>
+struct AdadeltaOp {  // optim.py:134-140
+  static constexpr int kSlots = 2;
+  CoupledWd<T> wd;
+  T neg_eta, eps, rho, one_minus_rho;
+  __device__ __forceinline__ void operator()(T& p, T g, T& sq, T& acc) const {
+    g = wd.apply(g, p);
+    sq = o_add(o_mul(rho, sq), o_mul(one_minus_rho, o_mul(g, g)));
+    T dx = o_mul(o_div(o_sqrt(o_add(acc, eps)), o_sqrt(o_add(sq, eps))), g);
+    acc = o_add(o_mul(rho, acc), o_mul(one_minus_rho, o_mul(dx, dx)));
+    p = o_add(p, o_mul(neg_eta, dx));
+  }
+};
+
+template <class T>
+struct AdamOp {  // optim.py:141-148
+  static constexpr int kSlots = 2;
+  CoupledWd<T> wd;
+  T neg_eta, eps, beta1, beta2, one_minus_beta1, one_minus_beta2, bc1, bc2;
+  __device__ __forceinline__ void operator()(T& p, T g, T& m, T& v) const {
+    g = wd.apply(g, p);
+    m = o_add(o_mul(beta1, m), o_mul(one_minus_beta1, g));
+    v = o_add(o_mul(beta2, v), o_mul(one_minus_beta2, o_mul(g, g)));
+    const T m_hat = o_div(m, bc1);
+    const T v_hat = o_div(v, bc2);
+    p = o_add(p, o_div(o_mul(neg_eta, m_hat), o_add(o_sqrt(v_hat), eps)));
+  }
+};
+
+// AdamW is not in the reference (SPEC.md:244 puts decoupled decay out of
+// scope).  It follows torch.optim.AdamW(foreach=False) step by step:
+//   param.mul_(1 - lr*wd); exp_avg.lerp_(grad, 1-beta1);
+//   exp_avg_sq.mul_(beta2).addcmul_(grad, grad, value=1-beta2);
+//   denom = exp_avg_sq.sqrt() / sqrt(bc2) + eps; param.addcdiv_(exp_avg, denom, -lr/bc1)
+template <class T>
+struct AdamWOp {
+  static constexpr int kSlots = 2;
+  T decay, w1, beta2, one_minus_beta2, bc2_sqrt, eps, neg_step;
+  bool decay_on, w1_small;
+  __device__ __forceinline__ void operator()(T& p, T g, T& m, T& v) const {
+    if (decay_on) p = o_mul(p, decay);
+    const T diff = o_sub(g, m);
+    m = w1_small ? o_fma(w1, diff, m)                        // lerp, weight < 0.5
+                 : o_fma(o_sub(w1, T(1)), diff, g);          // lerp, weight >= 0.5
+    v = o_add(o_mul(v, beta2), o_mul(o_mul(one_minus_beta2, g), g));
+    const T denom = o_add(o_div(o_sqrt(v), bc2_sqrt), eps);
+    p = o_add(p, o_div(o_mul(neg_step, m), denom));
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Tensor-list parameter block.
+// ---------------------------------------------------------------------------
+template <int CAP>
+struct MTParams {
+  void* p[CAP];
+  void* g[CAP];
+  void* s0[CAP];
+  void* s1[CAP];
+  void* sh[CAP];
+  int64_t n[CAP];
+  int32_t tile_end[CAP];  // inclusive prefix sum of tiles per tensor
+  int32_t count;
+};
+
+// 4-element vector loads/stores.
+__device__ __forceinline__ void ld4(const float* p, float (&v)[4]) {
+  const float4 t = *reinterpret_cast<const float4*>(p);
+  v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+}
+__device__ __forceinline__ void st4(float* p, const float (&v)[4]) {
+  *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+}
+__device__ __forceinline__ void ld4(const double* p, double (&v)[4]) {
+  const double2 a = reinterpret_cast<const double2*>(p)[0];
+  const double2 b = reinterpret_cast<const double2*>(p)[1];
+  v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+}
+__device__ __forceinline__ void st4(double* p, const double (&v)[4]) {
+  reinterpret_cast<double2*>(p)[0] = make_double2(v[0], v[1]);
+  reinterpret_cast<double2*>(p)[1] = make_double2(v[2], v[3]);
+}
+__device__ __forceinline__ void ld4(const __nv_bfloat16* p, float (&v)[4]) {
+  const uint2 t = *reinterpret_cast<const uint2*>(p);
+  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&t.x));
+  const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&t.y));
+  v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+}
+__device__ __forceinline__ void st4_bf16(__nv_bfloat16* p, const float (&v)[4]) {
+  __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]);
+  __nv_bfloat162 b = __floats2bfloat162_rn(v[2], v[3]);
+  uint2 t;
+  t.x = *reinterpret_cast<uint32_t*>(&a);
+  t.y = *reinterpret_cast<uint32_t*>(&b);
+  *reinterpret_cast<uint2*>(p) = t;
+}
+__device__ __forceinline__ void st4_bf16(__nv_bfloat16* p, const double (&v)[4]) {
+  const float f[4] = {(float)v[0], (float)v[1], (float)v[2], (float)v[3]};
+  st4_bf16(p, f);
+}
+__device__ __forceinline__ void st4_zero(float* p) { *reinterpret_cast<float4*>(p) = make_float4(0.f, 0.f, 0.f, 0.f); }
+__device__ __forceinline__ void st4_zero(double* p) {
+  reinterpret_cast<double2*>(p)[0] = make_double2(0.0, 0.0);
+  reinterpret_cast<double2*>(p)[1] = make_double2(0.0, 0.0);
+}
+__device__ __forceinline__ void st4_zero(__nv_bfloat16* p) { *reinterpret_cast<uint2*>(p) = make_uint2(0u, 0u); }
+
+template <class T> __device__ __forceinline__ T ld1(const T* p) { return *p; }
+__device__ __forceinline__ float ld1(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+template <class G> __device__ __forceinline__ void st1_zero(G* p) { *p = G(0); }
+__device__ __forceinline__ void st1_zero(__nv_bfloat16* p) { *p = __float2bfloat16_rn(0.f); }
+
+template <class T> struct GradVal { using type = T; };
+template <> struct GradVal<__nv_bfloat16> { using type = float; };
+
+__device__ __forceinline__ bool aligned(const void* p, unsigned a) {
+  return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0;
+}
+
+// One multi-tensor policy step.  T: param/state type; G: grad type.
+template <class Op, class T, class G, int CAP>
+__global__ void __launch_bounds__(kThreads)
+mt_step_kernel(const __grid_constant__ MTParams<CAP> mp, const Op op,
+               const float* __restrict__ gscale, uint32_t flags) {
+  using GV = typename GradVal<G>::type;
+  constexpr int kRound = sizeof(T) == 8 ? 2 : 4;  // vectors in flight per thread per round
+  const int total = mp.tile_end[mp.count - 1];
+  const bool zero_grad = (flags & OF_FLAG_ZERO_GRAD) != 0;
+  const bool shadow = (flags & OF_FLAG_SHADOW_BF16) != 0;
+  const bool has_scale = gscale != nullptr;
+  const T scale = has_scale ? T(*gscale) : T(1);
+  int ti = 0;
+  for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+    while (tile >= mp.tile_end[ti]) ++ti;
+    const int tfirst = ti ? mp.tile_end[ti - 1] : 0;
+    const int64_t base = static_cast<int64_t>(tile - tfirst) * kTile;
+    const int64_t rem = mp.n[ti] - base;
+    const int len = rem < kTile ? static_cast<int>(rem) : kTile;
+    T* p = static_cast<T*>(mp.p[ti]) + base;
+    G* g = static_cast<G*>(mp.g[ti]) + base;
+    T* s0 = Op::kSlots >= 1 ? static_cast<T*>(mp.s0[ti]) + base : nullptr;
+    T* s1 = Op::kSlots >= 2 ? static_cast<T*>(mp.s1[ti]) + base : nullptr;
+    __nv_bfloat16* sh = shadow ? static_cast<__nv_bfloat16*>(mp.sh[ti]) + base : nullptr;
+    const bool vec_ok = aligned(p, 16) && aligned(g, 4 * sizeof(G)) &&
+                        (Op::kSlots < 1 || aligned(s0, 16)) && (Op::kSlots < 2 || aligned(s1, 16)) &&
+                        (!shadow || aligned(sh, 8));
+    int scalar_from = 0;
+    if (vec_ok) {
+      const int nvec = len / kVec;
+#pragma unroll
+      for (int r = 0; r < kUnroll; r += kRound) {
+        T vp[kRound][4], v0[kRound][4], v1[kRound][4];
+        GV vg[kRound][4];
+#pragma unroll
+        for (int u = 0; u < kRound; ++u) {
+          const int j = threadIdx.x + (r + u) * kThreads;
+          if (j < nvec) {
+            ld4(p + 4 * j, vp[u]);
+            ld4(g + 4 * j, vg[u]);
+            if (Op::kSlots >= 1) ld4(s0 + 4 * j, v0[u]);
+            if (Op::kSlots >= 2) ld4(s1 + 4 * j, v1[u]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kRound; ++u) {
+          const int j = threadIdx.x + (r + u) * kThreads;
+          if (j < nvec) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              T gk = static_cast<T>(vg[u][k]);
+              if (has_scale) gk = o_mul(gk, scale);  // grad *= clip factor (optim.py:170)
+              op(vp[u][k], gk, v0[u][k], v1[u][k]);
+            }
+            st4(p + 4 * j, vp[u]);
+            if (Op::kSlots >= 1) st4(s0 + 4 * j, v0[u]);
+            if (Op::kSlots >= 2) st4(s1 + 4 * j, v1[u]);
+            if (zero_grad) st4_zero(g + 4 * j);
+            if (shadow) st4_bf16(sh + 4 * j, vp[u]);
+          }
+        }
+      }
+      scalar_from = nvec * kVec;
+    }
+    for (int e = scalar_from + threadIdx.x; e < len; e += kThreads) {
+      T pv = p[e];
+      T a = Op::kSlots >= 1 ? s0[e] : T(0);
+      T b = Op::kSlots >= 2 ? s1[e] : T(0);
+      T gk = static_cast<T>(ld1(g + e));
+      if (has_scale) gk = o_mul(gk, scale);
+      op(pv, gk, a, b);
+      p[e] = pv;
+      if (Op::kSlots >= 1) s0[e] = a;
+      if (Op::kSlots >= 2) s1[e] = b;
+      if (zero_grad) st1_zero(g + e);
+      if (shadow) sh[e] = __float2bfloat16_rn(static_cast<float>(pv));
+    }
+  }
+}
+
+// Sum of squares, per-CTA f64 partials (deterministic order within a CTA).
+template <class G, int CAP>
+__global__ void __launch_bounds__(kThreads)
+mt_sqnorm_kernel(const __grid_constant__ MTParams<CAP> mp, double* __restrict__ partials) {
+  const int total = mp.tile_end[mp.count - 1];
+  double acc = 0.0;
+  int ti = 0;
+  for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+    while (tile >= mp.tile_end[ti]) ++ti;
+    const int tfirst = ti ? mp.tile_end[ti - 1] : 0;
+    const int64_t base = static_cast<int64_t>(tile - tfirst) * kTile;
+    const int64_t rem = mp.n[ti] - base;
+    const int len = rem < kTile ? static_cast<int>(rem) : kTile;
+    const G* g = static_cast<const G*>(mp.g[ti]) + base;
+    for (int e = threadIdx.x; e < len; e += kThreads) {
+      const double x = static_cast<double>(ld1(g + e));
+      acc = __dadd_rn(acc, __dmul_rn(x, x));
+    }
+  }
+  __shared__ double red[kThreads / 32];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, off));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < kThreads / 32 ? red[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v = __dadd_rn(v, __shfl_down_sync(0xffffffffu, v, off));
+    if (threadIdx.x == 0) partials[blockIdx.x] = v;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+sqnorm_finalize_kernel(const double* __restrict__ partials, int n, double* out, int accumulate) {
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += kThreads) acc = __dadd_rn(acc, partials[i]);
+  __shared__ double red[kThreads / 32];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, off));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) s = __dadd_rn(s, red[w]);
+    *out = accumulate ? __dadd_rn(*out, s) : s;
+  }
+}
+
+__global__ void clip_coef_kernel(const double* sq, double max_norm, float* coef, double* factor_out) {
+  const double norm = __dsqrt_rn(*sq);                       // optim.py:165
+  const double factor = norm <= max_norm ? 1.0 : __ddiv_rn(max_norm, norm);  // optim.py:166-168
+  *coef = __double2float_rn(factor);                         // numpy casts the factor to f32
+  if (factor_out) *factor_out = factor;
+}
+
+// ---------------------------------------------------------------------------
+// Host side: validation, packing, dispatch.
+// ---------------------------------------------------------------------------
+int slots_of(int kind) {
+  switch (kind) {
+    case OF_SGD: return 0;
+    case OF_SGD_MOMENTUM: case OF_ADAGRAD: case OF_RMSPROP: return 1;
+    case OF_ADADELTA: case OF_ADAM: case OF_ADAMW: return 2;
+    default: return -1;
+  }
+}
+
+int validate_list(const of_tensor_list* l, int slots, bool need_shadow, bool grads_only) {
+  if (!l) return fail(OF_ERR_INVALID, "tensor list is NULL");
+  if (l->n < 0) return fail(OF_ERR_INVALID, "tensor list has n=%d < 0", l->n);
+  if (l->n == 0) return OF_OK;
+  if (l->param_dtype != OF_F32 && l->param_dtype != OF_F64)
+    return fail(OF_ERR_UNSUPPORTED, "param dtype %d not supported (f32, f64)", l->param_dtype);
+  if (!(l->grad_dtype == l->param_dtype || (l->grad_dtype == OF_BF16 && l->param_dtype == OF_F32)))
+    return fail(OF_ERR_UNSUPPORTED, "grad dtype %d with param dtype %d not supported",
+                l->grad_dtype, l->param_dtype);
+  if (!l->numel || !l->grad || (!grads_only && !l->param))
+    return fail(OF_ERR_INVALID, "tensor list is missing the param/grad/numel arrays");
+  if (!grads_only) {
+    if (slots >= 1 && !l->state0) return fail(OF_ERR_INVALID, "kind needs state0 (history slot 0)");
+    if (slots >= 2 && !l->state1) return fail(OF_ERR_INVALID, "kind needs state1 (history slot 1)");
+    if (need_shadow && !l->shadow) return fail(OF_ERR_INVALID, "OF_FLAG_SHADOW_BF16 needs shadow pointers");
+  }
+  for (int i = 0; i < l->n; ++i) {
+    if (l->numel[i] < 0) return fail(OF_ERR_INVALID, "tensor %d has numel %lld < 0", i, (long long)l->numel[i]);
+    if (l->numel[i] == 0) continue;
+    if (!l->grad[i]) return fail(OF_ERR_INVALID, "tensor %d has a NULL grad", i);
+    if (grads_only) continue;
+    if (!l->param[i]) return fail(OF_ERR_INVALID, "tensor %d has a NULL param", i);
+    if (slots >= 1 && !l->state0[i]) return fail(OF_ERR_INVALID, "tensor %d has a NULL state0", i);
+    if (slots >= 2 && !l->state1[i]) return fail(OF_ERR_INVALID, "tensor %d has a NULL state1", i);
+    if (need_shadow && !l->shadow[i]) return fail(OF_ERR_INVALID, "tensor %d has a NULL shadow", i);
+  }
+  return OF_OK;
+}
+
+// Packs tensors [first, first+count) into a parameter block; returns total tiles.
+template <int CAP>
+int64_t pack(const of_tensor_list* l, int first, int count, MTParams<CAP>& mp) {
+  int64_t tiles = 0;
+  mp.count = count;
+  for (int i = 0; i < count; ++i) {
+    const int k = first + i;
+    mp.p[i] = l->param ? l->param[k] : nullptr;
+    mp.g[i] = l->grad[k];
+    mp.s0[i] = l->state0 ? l->state0[k] : nullptr;
+    mp.s1[i] = l->state1 ? l->state1[k] : nullptr;
+    mp.sh[i] = l->shadow ? l->shadow[k] : nullptr;
+    mp.n[i] = l->numel[k];
+    tiles += (l->numel[k] + kTile - 1) / kTile;
+    mp.tile_end[i] = static_cast<int32_t>(tiles);
+  }
+  return tiles;
+}
+
+template <class Op, class T, class G, int CAP>
+int launch_step_chunk(const of_tensor_list* l, int first, int count, const Op& op,
+                      const float* gscale, uint32_t flags, cudaStream_t s) {
+  MTParams<CAP> mp;
+  const int64_t tiles = pack<CAP>(l, first, count, mp);
+  if (tiles == 0) return OF_OK;
+  if (tiles > INT32_MAX) return fail(OF_ERR_INVALID, "tensor list too large for one launch");
+  const int64_t cap = static_cast<int64_t>(sm_count()) * kCtasPerSm;
+  const int grid = static_cast<int>(tiles < cap ? tiles : cap);
+  mt_step_kernel<Op, T, G, CAP><<<grid, kThreads, 0, s>>>(mp, op, gscale, flags);
+  return check_launch("mt_step_kernel");
+}
+
+template <class Op, class T, class G>
+int launch_step(const of_tensor_list* l, const Op& op, const float* gscale, uint32_t flags,
+                cudaStream_t s) {
+  int first = 0;
+  while (first < l->n) {
+    const int left = l->n - first;
+    int st;
+    if (left <= 4) {
+      st = launch_step_chunk<Op, T, G, 4>(l, first, left, op, gscale, flags, s);
+      first += left;
+    } else if (left <= 16) {
+      st = launch_step_chunk<Op, T, G, 16>(l, first, left, op, gscale, flags, s);
+      first += left;
+    } else {
+      const int c = left < 64 ? left : 64;
+      st = launch_step_chunk<Op, T, G, 64>(l, first, c, op, gscale, flags, s);
+      first += c;
+    }
+    if (st != OF_OK) return st;
+  }
+  return OF_OK;
+}
+
+template <class T>
+CoupledWd<T> coupled(const of_hparams* hp) {
+  return CoupledWd<T>{static_cast<T>(hp->weight_decay), hp->weight_decay > 0.0};
+}
+
+template <class T, class G>
+int dispatch_kind(const of_tensor_list* l, const of_hparams* hp, const float* gscale,
+                  uint32_t flags, cudaStream_t s) {
+  const T neg_eta = static_cast<T>(-hp->eta);
+  switch (hp->kind) {
+    case OF_SGD: {
+      SgdOp<T> op{coupled<T>(hp), neg_eta};
+      return launch_step<SgdOp<T>, T, G>(l, op, gscale, flags, s);
+    }
+    case OF_SGD_MOMENTUM: {
+      SgdMomentumOp<T> op{coupled<T>(hp), neg_eta, static_cast<T>(hp->alpha)};
+      return launch_step<SgdMomentumOp<T>, T, G>(l, op, gscale, flags, s);
+    }
+    case OF_ADAGRAD: {
+      AdagradOp<T> op{coupled<T>(hp), neg_eta, static_cast<T>(hp->epsilon)};
+      return launch_step<AdagradOp<T>, T, G>(l, op, gscale, flags, s);
+    }
+    case OF_RMSPROP: {
+      RmspropOp<T> op{coupled<T>(hp), neg_eta, static_cast<T>(hp->epsilon),
+                      static_cast<T>(hp->rho), static_cast<T>(1.0 - hp->rho)};
+      return launch_step<RmspropOp<T>, T, G>(l, op, gscale, flags, s);
+    }
+    case OF_ADADELTA: {
+      AdadeltaOp<T> op{coupled<T>(hp), neg_eta, static_cast<T>(hp->epsilon),
+                       static_cast<T>(hp->rho), static_cast<T>(1.0 - hp->rho)};
+      return launch_step<AdadeltaOp<T>, T, G>(l, op, gscale, flags, s);
+    }
+    case OF_ADAM: {
+      AdamOp<T> op{coupled<T>(hp), neg_eta, static_cast<T>(hp->epsilon),
+                   static_cast<T>(hp->beta1), static_cast<T>(hp->beta2),
+                   static_cast<T>(1.0 - hp->beta1), static_cast<T>(1.0 - hp->beta2),
+                   static_cast<T>(hp->bias_correction1), static_cast<T>(hp->bias_correction2)};
+      return launch_step<AdamOp<T>, T, G>(l, op, gscale, flags, s);
+    }
+    case OF_ADAMW: {
+      const double w1 = 1.0 - hp->beta1;
+      AdamWOp<T> op{static_cast<T>(1.0 - hp->eta * hp->weight_decay), static_cast<T>(w1),
+                    static_cast<T>(hp->beta2), static_cast<T>(1.0 - hp->beta2),
+                    static_cast<T>(std::sqrt(hp->bias_correction2)), static_cast<T>(hp->epsilon),
+                    static_cast<T>(-(hp->eta / hp->bias_correction1)),
+                    hp->weight_decay != 0.0, std::fabs(w1) < 0.5};
+      return launch_step<AdamWOp<T>, T, G>(l, op, gscale, flags, s);
+    }
+    default:
+      return fail(OF_ERR_INVALID, "unknown optimizer kind %d", hp->kind);
+  }
+}
+
+template <class G, int CAP>
+int launch_sqnorm_chunk(const of_tensor_list* l, int first, int count, double* ws, int64_t ws_len,
+                        double* out, int accumulate, cudaStream_t s) {
+  MTParams<CAP> mp;
+  const int64_t tiles = pack<CAP>(l, first, count, mp);
+  if (tiles == 0) {
+    if (!accumulate) {
+      if (cudaMemsetAsync(out, 0, sizeof(double), s) != cudaSuccess)
+        return fail(OF_ERR_CUDA, "cudaMemsetAsync failed");
+    }
+    return OF_OK;
+  }
+  int64_t cap = static_cast<int64_t>(sm_count()) * 4;
+  if (cap > ws_len) cap = ws_len;
+  const int grid = static_cast<int>(tiles < cap ? tiles : cap);
+  mt_sqnorm_kernel<G, CAP><<<grid, kThreads, 0, s>>>(mp, ws);
+  int st = check_launch("mt_sqnorm_kernel");
+  if (st != OF_OK) return st;
+  sqnorm_finalize_kernel<<<1, kThreads, 0, s>>>(ws, grid, out, accumulate);
+  return check_launch("sqnorm_finalize_kernel");
+}
+
+template <class G>
+int launch_sqnorm(const of_tensor_list* l, double* ws, int64_t ws_len, double* out, int accumulate,
+                  cudaStream_t s) {
+  int first = 0;
+  do {
+    const int left = l->n - first;
+    const int c = left < 64 ? left : 64;
+    const int st = launch_sqnorm_chunk<G, 64>(l, first, c, ws, ws_len, out, accumulate, s);
+    if (st != OF_OK) return st;
+    accumulate = 1;
+    first += c;
+  } while (first < l->n);
+  return OF_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int of_abi_version(void) { return OF_ABI_VERSION; }
+
+const char* of_status_string(int status) {
+  switch (status) {
+    case OF_OK: return "ok";
+    case OF_ERR_INVALID: return "invalid argument";
+    case OF_ERR_UNSUPPORTED: return "unsupported combination";
+    case OF_ERR_CUDA: return "CUDA launch error";
+    default: return "unknown status";
+  }
+}
+
+const char* of_last_error(void) { return g_err; }
+
+uint64_t of_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+int of_policy_step_mt(const of_tensor_list* list, const of_hparams* hp,
+                      const float* grad_scale_dev, uint32_t flags, void* stream) {
+  g_err[0] = '\0';
+  if (!hp) return fail(OF_ERR_INVALID, "hparams is NULL");
+  const int slots = slots_of(hp->kind);
+  if (slots < 0) return fail(OF_ERR_INVALID, "unknown optimizer kind %d", hp->kind);
+  if (flags & ~(OF_FLAG_ZERO_GRAD | OF_FLAG_SHADOW_BF16))
+    return fail(OF_ERR_INVALID, "unknown flags 0x%x", flags);
+  if (!(hp->eta > 0.0)) return fail(OF_ERR_INVALID, "step size must be > 0, got %g", hp->eta);
+  if ((hp->kind == OF_ADAM || hp->kind == OF_ADAMW) &&
+      (hp->bias_correction1 == 0.0 || hp->bias_correction2 == 0.0))
+    return fail(OF_ERR_INVALID, "adam bias corrections must be non-zero (step index t >= 1)");
+  int st = validate_list(list, slots, (flags & OF_FLAG_SHADOW_BF16) != 0, false);
+  if (st != OF_OK || list->n == 0) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (list->param_dtype == OF_F64) return dispatch_kind<double, double>(list, hp, grad_scale_dev, flags, s);
+  if (list->grad_dtype == OF_BF16) return dispatch_kind<float, __nv_bfloat16>(list, hp, grad_scale_dev, flags, s);
+  return dispatch_kind<float, float>(list, hp, grad_scale_dev, flags, s);
+}
+
+int of_sgdm_mt(const of_tensor_list* list, double eta, double alpha, double weight_decay,
+               const float* grad_scale_dev, uint32_t flags, void* stream) {
+  of_hparams hp;
+  memset(&hp, 0, sizeof(hp));
+  hp.kind = OF_SGD_MOMENTUM;
+  hp.eta = eta;
+  hp.alpha = alpha;
+  hp.weight_decay = weight_decay;
+  return of_policy_step_mt(list, &hp, grad_scale_dev, flags, stream);
+}
+
+int of_adam_mt(const of_tensor_list* list, double eta, double beta1, double beta2, double epsilon,
+               double weight_decay, double bias_correction1, double bias_correction2,
+               int decoupled_weight_decay, const float* grad_scale_dev, uint32_t flags,
+               void* stream) {
+  of_hparams hp;
+  memset(&hp, 0, sizeof(hp));
+  hp.kind = decoupled_weight_decay ? OF_ADAMW : OF_ADAM;
+  hp.eta = eta;
+  hp.beta1 = beta1;
+  hp.beta2 = beta2;
+  hp.epsilon = epsilon;
+  hp.weight_decay = weight_decay;
+  hp.bias_correction1 = bias_correction1;
+  hp.bias_correction2 = bias_correction2;
+  return of_policy_step_mt(list, &hp, grad_scale_dev, flags, stream);
+}
+
+int64_t of_sqnorm_workspace_len(void) { return kSqnormWorkspace; }
+
+int of_sqnorm_mt(const of_tensor_list* list, double* workspace_dev, int64_t workspace_len,
+                 double* out_dev, int accumulate, void* stream) {
+  g_err[0] = '\0';
+  if (!workspace_dev || workspace_len < 1) return fail(OF_ERR_INVALID, "sqnorm needs a workspace");
+  if (!out_dev) return fail(OF_ERR_INVALID, "sqnorm output pointer is NULL");
+  int st = validate_list(list, 0, false, true);
+  if (st != OF_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (list->n == 0) {
+    if (!accumulate && cudaMemsetAsync(out_dev, 0, sizeof(double), s) != cudaSuccess)
+      return fail(OF_ERR_CUDA, "cudaMemsetAsync failed");
+    return OF_OK;
+  }
+  switch (list->grad_dtype) {
+    case OF_F32: return launch_sqnorm<float>(list, workspace_dev, workspace_len, out_dev, accumulate, s);
+    case OF_F64: return launch_sqnorm<double>(list, workspace_dev, workspace_len, out_dev, accumulate, s);
+    case OF_BF16: return launch_sqnorm<__nv_bfloat16>(list, workspace_dev, workspace_len, out_dev, accumulate, s);
+    default: return fail(OF_ERR_UNSUPPORTED, "grad dtype %d", list->grad_dtype);
+  }
+}
+
+int of_clip_coef(const double* sqnorm_dev, double max_norm, float* coef_dev, double* factor_dev,
+                 void* stream) {
+  g_err[0] = '\0';
+  if (!sqnorm_dev || !coef_dev) return fail(OF_ERR_INVALID, "clip_coef needs sqnorm and coef pointers");
+  if (!(max_norm >= 0.0)) return fail(OF_ERR_INVALID, "max_norm must be >= 0, got %g", max_norm);
+  clip_coef_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(sqnorm_dev, max_norm, coef_dev, factor_dev);
+  return check_launch("clip_coef_kernel");
+}
+
+}  // extern "C"

@@ -1,0 +1,106 @@
+"""Thin host wrappers around the C ABI: tensor lists and launches.
+
+A ``TensorList`` is the host-memory ``of_tensor_list`` for one fixed set of
+parameters (a layer, a bucket, or the whole model); its ctypes pointer arrays
+are allocated once and only the device pointers are rewritten per launch, so
+issuing a multi-tensor update from a hook costs one ctypes call.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _native as nat
+from .errors import ConfigError
+
+_DTYPE_CODES = {torch.float32: nat.OF_F32, torch.float64: nat.OF_F64,
+                torch.bfloat16: nat.OF_BF16}
+
+
+def dtype_code(dt: torch.dtype) -> int:
+    try:
+        return _DTYPE_CODES[dt]
+    except KeyError:
+        raise ConfigError(f"dtype {dt} is not supported by the update kernels "
+                          "(float32, float64; bfloat16 gradients into float32 params)")
+
+
+class TensorList:
+    """Cached ``of_tensor_list`` with room for ``n`` tensors."""
+
+    __slots__ = ("n", "param", "grad", "state0", "state1", "shadow", "numel", "struct", "ref")
+
+    def __init__(self, n: int):
+        self.n = n
+        self.param = (ctypes.c_void_p * max(n, 1))()
+        self.grad = (ctypes.c_void_p * max(n, 1))()
+        self.state0 = (ctypes.c_void_p * max(n, 1))()
+        self.state1 = (ctypes.c_void_p * max(n, 1))()
+        self.shadow = (ctypes.c_void_p * max(n, 1))()
+        self.numel = (ctypes.c_int64 * max(n, 1))()
+        pp = nat._PP
+        self.struct = nat.OfTensorList(
+            n, nat.OF_F32, nat.OF_F32, 0,
+            ctypes.cast(self.param, pp), ctypes.cast(self.grad, pp),
+            ctypes.cast(self.state0, pp), ctypes.cast(self.state1, pp),
+            ctypes.cast(self.shadow, pp), ctypes.cast(self.numel, ctypes.POINTER(ctypes.c_int64)))
+        self.ref = ctypes.byref(self.struct)
+
+    def set_dtypes(self, param_dtype: torch.dtype, grad_dtype: torch.dtype) -> None:
+        self.struct.param_dtype = dtype_code(param_dtype)
+        self.struct.grad_dtype = dtype_code(grad_dtype)
+
+    def set(self, i: int, param, grad, state0=None, state1=None, shadow=None) -> None:
+        self.param[i] = param.data_ptr() if param is not None else None
+        self.grad[i] = grad.data_ptr()
+        self.state0[i] = state0.data_ptr() if state0 is not None else None
+        self.state1[i] = state1.data_ptr() if state1 is not None else None
+        self.shadow[i] = shadow.data_ptr() if shadow is not None else None
+        self.numel[i] = grad.numel()
+
+
+def hparams(kind: str, eta: float, alpha: float, weight_decay: float, epsilon: float,
+            beta1: float, beta2: float, rho: float, t: int) -> nat.OfHparams:
+    """of_hparams for step index t; bias corrections in double (optim.py:145-146)."""
+    bc1 = bc2 = 1.0
+    if kind in ("adam", "adamw"):
+        bc1 = 1 - beta1 ** t
+        bc2 = 1 - beta2 ** t
+    return nat.OfHparams(nat.KIND_CODES[kind], 0, eta, alpha, weight_decay, epsilon, beta1,
+                         beta2, rho, bc1, bc2)
+
+
+def policy_step(tl: TensorList, hp: nat.OfHparams, grad_scale, flags: int, stream) -> None:
+    """of_policy_step_mt on ``stream`` (a torch.cuda.Stream or raw handle)."""
+    gs = grad_scale.data_ptr() if grad_scale is not None else None
+    st = nat.lib().of_policy_step_mt(tl.ref, ctypes.byref(hp), gs, flags, _handle(stream))
+    if st:
+        nat.check(st, "of_policy_step_mt")
+
+
+def sqnorm(tl: TensorList, workspace: torch.Tensor, out: torch.Tensor, accumulate: bool,
+           stream) -> None:
+    st = nat.lib().of_sqnorm_mt(tl.ref, workspace.data_ptr(), workspace.numel(), out.data_ptr(),
+                                int(accumulate), _handle(stream))
+    nat.check(st, "of_sqnorm_mt")
+
+
+def clip_coef(sq: torch.Tensor, max_norm: float, coef: torch.Tensor, factor: torch.Tensor,
+              stream) -> None:
+    st = nat.lib().of_clip_coef(sq.data_ptr(), float(max_norm), coef.data_ptr(),
+                                factor.data_ptr(), _handle(stream))
+    nat.check(st, "of_clip_coef")
+
+
+def sqnorm_workspace_len() -> int:
+    return int(nat.lib().of_sqnorm_workspace_len())
+
+
+def _handle(stream):
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream

@@ -1,0 +1,307 @@
+"""Update policies on the GPU: the reference's OptimizerPolicy, executed by the
+sm_100a multi-tensor kernels.
+
+Mirrors /root/reference/pkg/src/optfuse/optim.py:
+  * ``OptimizerPolicy`` -- same fields, defaults, validation (optim.py:34-72);
+  * ``OptimizerPolicy.step(param, step_t=None, trace=None)`` -- same contract
+    (optim.py:74-115): newton and count != 0 raise before anything is touched,
+    history is allocated lazily as zeros, the gradient is reset (zeroed in the
+    kernel, or released when ``grad_reset="none"``), the parameter is updated
+    in place;
+  * ``clip_by_global_norm(graph, max_norm)`` (optim.py:151-172) -- the squared
+    norm is reduced on the device; the factor is *not* applied in a second
+    pass over the gradients but carried as a device scalar into the next step
+    of every parameter (bitwise the same as scaling the gradient first).
+
+B200 additions: ``step_params`` updates a whole list of parameters in one
+kernel launch (the per-layer / per-bucket unit of the fused schedules), the
+``adamw`` kind (torch.optim.AdamW semantics, not in the reference), and the
+``stream`` argument that the backward-fusion engine uses to issue updates on
+its side stream.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from . import kernels
+from . import trace as tr
+from .errors import ConfigError, NumericError, SchedulingContractError, StateError
+
+KINDS = ("sgd", "sgd-momentum", "newton", "adagrad", "rmsprop", "adadelta", "adam", "adamw")
+
+_HISTORY_SLOTS = {
+    "sgd": (),
+    "sgd-momentum": ("momentum",),
+    "adagrad": ("sum_sq",),
+    "rmsprop": ("square_avg",),
+    "adadelta": ("square_avg", "acc_delta"),
+    "adam": ("exp_avg", "exp_avg_sq"),
+    "adamw": ("exp_avg", "exp_avg_sq"),
+}
+
+GRAD_RESETS = ("zero", "none")
+
+
+@dataclass
+class OptimizerPolicy:
+    """One update rule and its constants (optim.py:34-72).
+
+    ``t`` counts begun iterations and feeds the Adam bias corrections; the
+    schedulers advance it exactly once per iteration.  ``grad_reset`` chooses
+    how a step resets the gradient: ``"zero"`` (reference semantics,
+    optim.py:111 -- the kernel writes zeros, gradients stay allocated) or
+    ``"none"`` (the gradient tensor is released after the step, so the next
+    backward's AccumulateGrad steals its input instead of adding into it).
+    """
+
+    kind: str = "sgd"
+    eta: float = 0.01
+    alpha: float = 0.9
+    weight_decay: float = 0.0
+    epsilon: float = 1e-8
+    beta1: float = 0.9
+    beta2: float = 0.999
+    rho: float = 0.9
+    clip_norm: float | None = None
+    t: int = 0
+    grad_reset: str = "zero"
+    _lists: dict = field(default_factory=dict, repr=False, compare=False)
+    _hp_cache: tuple = field(default=(None, None), repr=False, compare=False)
+
+    def __post_init__(self):
+        if self.kind not in KINDS:
+            raise ConfigError(f"unknown optimizer {self.kind!r}, expected one of {KINDS}")
+        if self.eta <= 0:
+            raise ConfigError(f"step size must be > 0, got {self.eta}")
+        if not 0 <= self.alpha < 1:
+            raise ConfigError(f"momentum decay must be in [0, 1), got {self.alpha}")
+        if self.weight_decay < 0:
+            raise ConfigError(f"weight decay must be >= 0, got {self.weight_decay}")
+        if self.grad_reset not in GRAD_RESETS:
+            raise ConfigError(f"grad_reset must be one of {GRAD_RESETS}, got {self.grad_reset!r}")
+
+    @property
+    def requires_global_info(self) -> bool:
+        """True iff no parameter may be updated before all gradients exist."""
+        return self.clip_norm is not None or self.kind == "newton"
+
+    def history_slots(self) -> tuple:
+        return _HISTORY_SLOTS.get(self.kind, ())
+
+    def begin_iteration(self) -> None:
+        self.t += 1
+
+    # -- single-parameter API (the reference's plugin boundary) -------------
+
+    def step(self, param, step_t: int | None = None, trace: tr.ScheduleTrace | None = None,
+             stream=None) -> None:
+        """Apply this policy's update to one parameter, in place."""
+        self.step_params((param,), step_t=step_t, trace=trace, stream=stream)
+
+    # -- multi-tensor API (one kernel launch) --------------------------------
+
+    def check_steppable(self, params) -> None:
+        """The contract checks of optim.py:82-87; raises before any mutation."""
+        if self.kind == "newton":
+            raise ConfigError("newton needs the full Hessian and has no per-parameter step")
+        for p in params:
+            if p.count != 0:
+                raise SchedulingContractError(
+                    f"parameter {p.id} still has {p.count} pending gradient contributions")
+            if not p._layout_ok:
+                _check_layout(p, p.value.grad)
+
+    def step_params(self, params, step_t: int | None = None,
+                    trace: tr.ScheduleTrace | None = None, stream=None,
+                    hold: list | None = None) -> None:
+        """Update every parameter of ``params`` with one multi-tensor launch.
+
+        Arithmetic per parameter is exactly ``step`` (parameters are
+        independent, optim.py:3-5).  ``stream``: CUDA stream to launch on
+        (default: current).  ``hold``: when given and ``grad_reset == "none"``,
+        released gradient tensors are appended to it so the caller can keep
+        them alive until ``stream`` has been joined.
+        """
+        params = tuple(params)
+        if not params:
+            return
+        self.check_steppable(params)
+        t = self.t if step_t is None else step_t
+        if self.kind in ("adam", "adamw") and t < 1:
+            raise StateError(f"{self.kind} step needs step index t >= 1 (call begin_iteration)")
+        slots = _HISTORY_SLOTS[self.kind]
+        # group by gradient scale (global-norm clip factor) -- normally one group
+        scale = params[0]._grad_scale
+        if any(p._grad_scale is not scale for p in params):
+            by_scale: dict = {}
+            for p in params:
+                by_scale.setdefault(id(p._grad_scale), []).append(p)
+            for group in by_scale.values():
+                self.step_params(group, step_t=step_t, trace=trace, stream=stream, hold=hold)
+            return
+
+        key = tuple(id(p) for p in params)
+        tl = self._lists.get(key)
+        if tl is None:
+            tl = kernels.TensorList(len(params))
+            self._lists[key] = tl
+        zero = self.grad_reset == "zero"
+        self.prepare(params)
+        s_a = slots[0] if slots else None
+        s_b = slots[1] if len(slots) > 1 else None
+        for i, p in enumerate(params):
+            v = p.value
+            h = p.history
+            tl.set(i, v, v.grad, h[s_a] if s_a else None, h[s_b] if s_b else None, None)
+        p0 = params[0].value
+        tl.set_dtypes(p0.dtype, p0.grad.dtype)
+        kernels.policy_step(tl, self._hparams(t), scale,
+                            nat.OF_FLAG_ZERO_GRAD if zero else 0, stream)
+        if trace is not None:
+            for p in params:
+                trace.record_mem(tr.PARAM, p.id, tr.READ)
+                trace.record_mem(tr.GRAD, p.id, tr.READ)
+                if slots:
+                    trace.record_mem(tr.HISTORY, p.id, tr.READ)
+                    trace.record_mem(tr.HISTORY, p.id, tr.WRITE)
+                trace.record_mem(tr.GRAD, p.id, tr.WRITE)
+                trace.record_mem(tr.PARAM, p.id, tr.WRITE)
+        for p in params:
+            p.pending = False
+            p._grad_scale = None
+            if not zero:
+                if hold is not None and p.value.grad is not None:
+                    hold.append(p.value.grad)
+                p.value.grad = None
+
+    def prepare(self, params, hold: list | None = None) -> None:
+        """Allocate, on the current stream, what a step of ``params`` needs:
+        zero history slots on first use (optim.py:90-94) and a zero gradient
+        for a parameter that received no contribution this iteration (the
+        reference steps every parameter, with g = 0, schedule.py:87)."""
+        slots = _HISTORY_SLOTS[self.kind]
+        for p in params:
+            v = p.value
+            if v.grad is None:
+                v.grad = torch.zeros_like(v)
+            h = p.history
+            if len(h) < len(slots):
+                for name in slots:
+                    if name not in h:
+                        h[name] = torch.zeros_like(v, memory_format=torch.preserve_format)
+
+    def _hparams(self, t: int) -> nat.OfHparams:
+        key = (t, self.kind, self.eta, self.alpha, self.weight_decay, self.epsilon,
+               self.beta1, self.beta2, self.rho)
+        cached_key, hp = self._hp_cache
+        if cached_key != key:
+            hp = kernels.hparams(self.kind, self.eta, self.alpha, self.weight_decay, self.epsilon,
+                                 self.beta1, self.beta2, self.rho, t)
+            self._hp_cache = (key, hp)
+        return hp
+
+
+def bytes_per_element(kind: str, param_itemsize: int = 4, grad_itemsize: int | None = None,
+                      shadow: bool = False) -> int:
+    """Algorithmic HBM bytes of one element update: read
+    theta, grad and every history slot; write theta and every slot (+ a bf16
+    shadow).  Gradient zeroing is not counted."""
+    slots = len(_HISTORY_SLOTS[kind])
+    g = param_itemsize if grad_itemsize is None else grad_itemsize
+    return param_itemsize * (2 + 2 * slots) + g + (2 if shadow else 0)
+
+
+def algorithmic_bytes(kind: str, params) -> int:
+    total = 0
+    for p in params:
+        v = p.value if hasattr(p, "value") else p
+        total += v.numel() * bytes_per_element(kind, v.element_size())
+    return total
+
+
+def _check_layout(p, g) -> None:
+    """Parameter, gradient and (zeros_like) history must share one dense
+    layout: the kernels walk the three buffers in storage order."""
+    v = p.value
+    if not v.is_cuda:
+        raise ConfigError(f"parameter {p.id} is on {v.device}; the update kernels run on CUDA only")
+    if v.dtype not in (torch.float32, torch.float64):
+        raise ConfigError(f"parameter {p.id} has dtype {v.dtype}; expected float32 or float64")
+    if not (v.is_contiguous() or v.is_contiguous(memory_format=torch.channels_last)):
+        raise ConfigError(f"parameter {p.id} is not dense; the update kernels need dense storage")
+    if g is None:
+        return  # checked again once a gradient exists
+    if g.shape != v.shape or g.stride() != v.stride() or g.device != v.device:
+        raise ConfigError(f"parameter {p.id}: gradient layout {tuple(g.stride())} on {g.device} "
+                          f"differs from parameter layout {tuple(v.stride())} on {v.device}")
+    if not (g.dtype == v.dtype or (g.dtype == torch.bfloat16 and v.dtype == torch.float32)):
+        raise ConfigError(f"parameter {p.id}: gradient dtype {g.dtype} with parameter {v.dtype}")
+    p._layout_ok = True
+
+
+def clip_by_global_norm(graph, max_norm: float, trace: tr.ScheduleTrace | None = None,
+                        stream=None) -> torch.Tensor:
+    """Global-norm clip (optim.py:151-172) as a device reduction.
+
+    Returns the clip factor as a 0-dim float64 CUDA tensor (1.0 when nothing
+    is clipped); ``float(result)`` gives the reference's return value (and
+    synchronises).  The factor is attached to every parameter and folded into
+    its next update -- the reference's in-place ``grad *= factor`` without a
+    second pass over the gradients.
+    """
+    params = graph.parameters
+    grads = [p.value.grad for p in params]
+    live = [g for g in grads if g is not None]
+    dev = params[0].value.device
+    sq = torch.empty((), dtype=torch.float64, device=dev)
+    factor = torch.empty((), dtype=torch.float64, device=dev)
+    coef = torch.empty((), dtype=torch.float32, device=dev)
+    ws = torch.empty(kernels.sqnorm_workspace_len(), dtype=torch.float64, device=dev)
+    if trace is not None:
+        for p in params:
+            trace.record_mem(tr.GRAD, p.id, tr.READ)
+    first = True
+    by_dtype: dict = {}
+    for g in live:
+        by_dtype.setdefault(g.dtype, []).append(g)
+    if not by_dtype:
+        sq.zero_()
+    for dt, gl in by_dtype.items():
+        tl = kernels.TensorList(len(gl))
+        for i, g in enumerate(gl):
+            tl.set(i, None, g)
+        tl.set_dtypes(dt if dt != torch.bfloat16 else torch.float32, dt)
+        kernels.sqnorm(tl, ws, sq, accumulate=not first, stream=stream)
+        first = False
+    kernels.clip_coef(sq, max_norm, coef, factor, stream)
+    for p in params:
+        p._grad_scale = coef
+        if trace is not None:
+            trace.record_mem(tr.GRAD, p.id, tr.WRITE)
+    return factor
+
+
+def newton_step(theta, grad_fn, hessian_fn, eta: float = 1.0):
+    """Full-Hessian toy validator (optim.py:175-194).  Not on the fused path:
+    it couples every coordinate, so no schedule can host it (schedule.py:62-64);
+    kept for API completeness and evaluated on the host in float64."""
+    th = np.asarray(theta.detach().cpu().numpy() if isinstance(theta, torch.Tensor) else theta)
+    d = th.size
+    if d > 16:
+        raise ConfigError(f"newton step is limited to dimension <= 16, got {d}")
+    g = np.asarray(grad_fn(th.copy()), dtype=np.float64).reshape(d)
+    h = np.asarray(hessian_fn(th.copy()), dtype=np.float64).reshape(d, d)
+    try:
+        direction = np.linalg.solve(h, g)
+    except np.linalg.LinAlgError as e:
+        raise NumericError(f"Hessian is singular: {e}") from e
+    if not np.all(np.isfinite(direction)):
+        raise NumericError("Hessian solve produced non-finite values")
+    new = th.astype(np.float64).reshape(d) - eta * direction
+    out = new.astype(th.dtype).reshape(th.shape)
+    return torch.from_numpy(out) if isinstance(theta, torch.Tensor) else out

@@ -1,0 +1,273 @@
+"""Kernel parity on the GPU: the sm_100a update kernels against the pinned
+oracle (bit-exact for the reference kinds) and torch AdamW (tolerance)."""
+
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2104_00237_b200 as of
+from paper_2104_00237_b200 import _native as nat
+from paper_2104_00237_b200 import kernels
+from oracle import optim_ref
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+KINDS = optim_ref.KINDS
+ETA = {"sgd": 0.01, "sgd-momentum": 0.01, "adagrad": 0.01, "rmsprop": 1e-3,
+       "adadelta": 1.0, "adam": 1e-3}
+TDT = {"f32": torch.float32, "f64": torch.float64}
+
+
+def _param(arr, pid=0):
+    return of.Parameter(pid, torch.nn.Parameter(torch.from_numpy(arr.copy()).to(DEV)))
+
+
+@pytest.mark.parametrize("kind", KINDS)
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+@pytest.mark.parametrize("wd", [0.0, 1e-2])
+def test_golden_policy_trajectories(policy_golden, kind, prec, wd):
+    key = f"{kind}|{prec}|wd{wd}"
+    p = _param(policy_golden[key + "|theta0"])
+    grads = policy_golden[key + "|grads"]
+    traj = policy_golden[key + "|traj"]
+    pol = of.OptimizerPolicy(kind=kind, eta=ETA[kind], weight_decay=wd)
+    for s in range(grads.shape[0]):
+        pol.begin_iteration()
+        p.value.grad = torch.from_numpy(grads[s].copy()).to(DEV)
+        pol.step(p)
+        got = p.value.detach().cpu().numpy()
+        assert got.tobytes() == traj[s].tobytes(), f"step {s + 1}: max diff {np.abs(got - traj[s]).max()}"
+        assert not p.value.grad.any(), "grad must be zero after the step (optim.py:111)"
+    for name in pol.history_slots():
+        assert p.history[name].cpu().numpy().tobytes() == policy_golden[key + "|slot|" + name].tobytes()
+
+
+def _resnet18_shapes():
+    g = of.build_classifier("resnet18_cifar", device="cpu")
+    return [tuple(p.value.shape) for p in g.parameters]
+
+
+@pytest.mark.parametrize("kind,hp", [("sgd-momentum", dict(eta=0.1, alpha=0.9, weight_decay=5e-4)),
+                                     ("adam", dict(eta=1e-3, weight_decay=1e-4)),
+                                     ("adadelta", dict(eta=1.0, weight_decay=1e-4))])
+def test_multi_tensor_resnet18_shapes_bitwise(kind, hp):
+    """100 injected-gradient steps over the 62 ResNet-18/CIFAR tensors (11.17 M
+    elements, one multi-tensor launch per step) equal the oracle bit for bit."""
+    shapes = _resnet18_shapes()
+    rng = np.random.default_rng(0)
+    thetas = [(rng.standard_normal(int(np.prod(s))) * 0.05).astype(np.float32) for s in shapes]
+    params = [_param(t, i) for i, t in enumerate(thetas)]
+    pol = of.OptimizerPolicy(kind=kind, **hp)
+    ref_slots = [dict() for _ in shapes]
+    h = optim_ref.Hyper(kind=kind, **hp)
+    steps = 100 if kind == "sgd-momentum" else 12
+    for s in range(steps):
+        pol.begin_iteration()
+        grads = [(rng.standard_normal(t.size) * 0.01).astype(np.float32) for t in thetas]
+        for p, g in zip(params, grads):
+            p.value.grad = torch.from_numpy(g).to(DEV)
+        pol.step_params(reversed(params))
+        for t, g, sl in zip(thetas, grads, ref_slots):
+            optim_ref.step(kind, h, t, g, sl, s + 1)
+    for p, t, sl in zip(params, thetas, ref_slots):
+        assert p.value.detach().cpu().numpy().reshape(-1).tobytes() == t.tobytes()
+        for name in pol.history_slots():
+            assert p.history[name].cpu().numpy().reshape(-1).tobytes() == sl[name].tobytes()
+
+
+@pytest.mark.parametrize("offset", [0, 1, 2, 3])
+@pytest.mark.parametrize("kind", ["sgd-momentum", "adam"])
+def test_unaligned_and_ragged_views(offset, kind):
+    """Parameters that are views at unaligned offsets of one buffer, with sizes
+    that are not multiples of the vector width or tile (scalar path + tails)."""
+    sizes = [1, 3, 4, 5, 4095, 4096, 4097, 70001]
+    total = sum(sizes) + offset
+    rng = np.random.default_rng(offset)
+    flat_p = torch.from_numpy(rng.standard_normal(total).astype(np.float32)).to(DEV)
+    flat_g = torch.zeros(total, device=DEV)
+    params, thetas, o = [], [], offset
+    for i, n in enumerate(sizes):
+        v = torch.nn.Parameter(flat_p[o:o + n])
+        params.append(of.Parameter(i, v))
+        thetas.append(flat_p[o:o + n].cpu().numpy().copy())
+        o += n
+    pol = of.OptimizerPolicy(kind=kind, eta=1e-2)
+    h = optim_ref.Hyper(kind=kind, eta=1e-2)
+    slots = [dict() for _ in sizes]
+    o = offset
+    views = []
+    for n in sizes:
+        views.append(flat_g[o:o + n])
+        o += n
+    for s in range(5):
+        pol.begin_iteration()
+        for p, v in zip(params, views):
+            v.copy_(torch.randn(v.numel(), device=DEV))
+            p.value.grad = v
+        host_g = [v.cpu().numpy().copy() for v in views]
+        pol.step_params(params)
+        for t, g, sl in zip(thetas, host_g, slots):
+            optim_ref.step(kind, h, t, g, sl, s + 1)
+    for p, t in zip(params, thetas):
+        assert p.value.detach().cpu().numpy().tobytes() == t.tobytes()
+    assert not flat_g.any()
+
+
+def test_many_tensors_chunked_launches():
+    """> 64 tensors (several launches per step) and tiny tensors."""
+    rng = np.random.default_rng(3)
+    arrs = [rng.standard_normal(int(n)).astype(np.float32) for n in rng.integers(1, 300, 150)]
+    params = [_param(a, i) for i, a in enumerate(arrs)]
+    pol = of.OptimizerPolicy("adam", eta=1e-3)
+    h = optim_ref.Hyper(kind="adam", eta=1e-3)
+    slots = [dict() for _ in arrs]
+    for s in range(3):
+        pol.begin_iteration()
+        gs = [rng.standard_normal(a.size).astype(np.float32) for a in arrs]
+        for p, g in zip(params, gs):
+            p.value.grad = torch.from_numpy(g).to(DEV)
+        n0 = nat.launch_count()
+        pol.step_params(params)
+        assert nat.launch_count() - n0 == 3  # 64 + 64 + 22
+        for a, g, sl in zip(arrs, gs, slots):
+            optim_ref.step("adam", h, a, g, sl, s + 1)
+    for p, a in zip(params, arrs):
+        assert p.value.detach().cpu().numpy().tobytes() == a.tobytes()
+
+
+def test_grad_reset_none_releases_gradients():
+    rng = np.random.default_rng(5)
+    a = rng.standard_normal(1000).astype(np.float32)
+    p = _param(a)
+    pol = of.OptimizerPolicy("sgd-momentum", eta=0.1, grad_reset="none")
+    h = optim_ref.Hyper(kind="sgd-momentum", eta=0.1)
+    sl = {}
+    for s in range(3):
+        pol.begin_iteration()
+        g = rng.standard_normal(1000).astype(np.float32)
+        p.value.grad = torch.from_numpy(g.copy()).to(DEV)
+        pol.step(p)
+        assert p.value.grad is None
+        optim_ref.step("sgd-momentum", h, a, g, sl, s + 1)
+    assert p.value.detach().cpu().numpy().tobytes() == a.tobytes()
+
+
+def test_missing_grad_steps_with_zero_gradient():
+    """The reference steps every parameter, even one without contributions."""
+    a = np.linspace(-1, 1, 77).astype(np.float32)
+    p = _param(a)
+    pol = of.OptimizerPolicy("sgd-momentum", eta=0.1, weight_decay=0.01)
+    pol.begin_iteration()
+    pol.step(p)
+    optim_ref.step("sgd-momentum", optim_ref.Hyper("sgd-momentum", eta=0.1, weight_decay=0.01),
+                   a, np.zeros_like(a), {}, 1)
+    assert p.value.detach().cpu().numpy().tobytes() == a.tobytes()
+
+
+def _raw_list(ps, gs, s0=None, s1=None, sh=None):
+    tl = kernels.TensorList(len(ps))
+    for i in range(len(ps)):
+        tl.set(i, ps[i], gs[i], s0[i] if s0 else None, s1[i] if s1 else None,
+               sh[i] if sh else None)
+    tl.set_dtypes(ps[0].dtype, gs[0].dtype)
+    return tl
+
+
+def test_bf16_grads_fp32_master_and_bf16_shadow():
+    """Mixed precision: bf16 gradients into fp32 master weights, bf16 shadow
+    written in the same pass; equals the fp32 kernel fed the upcast grads."""
+    torch.manual_seed(0)
+    n = [5000, 3, 131073]
+    master = [torch.randn(k, device=DEV) for k in n]
+    m = [torch.zeros(k, device=DEV) for k in n]
+    v = [torch.zeros(k, device=DEV) for k in n]
+    shadow = [torch.empty(k, device=DEV, dtype=torch.bfloat16) for k in n]
+    ref_p = [x.cpu().numpy().copy() for x in master]
+    ref_s = [dict() for _ in n]
+    h = optim_ref.Hyper(kind="adam", eta=1e-3, weight_decay=1e-4)
+    for t in range(1, 4):
+        g16 = [torch.randn(k, device=DEV).to(torch.bfloat16) for k in n]
+        host_g = [g.float().cpu().numpy() for g in g16]
+        tl = _raw_list(master, g16, m, v, shadow)
+        hp = kernels.hparams("adam", 1e-3, 0.9, 1e-4, 1e-8, 0.9, 0.999, 0.9, t)
+        kernels.policy_step(tl, hp, None, nat.OF_FLAG_SHADOW_BF16 | nat.OF_FLAG_ZERO_GRAD, None)
+        for i, g in enumerate(g16):
+            assert not g.any()
+        for i in range(len(n)):
+            optim_ref.step("adam", h, ref_p[i], host_g[i], ref_s[i], t)
+    for i in range(len(n)):
+        assert master[i].cpu().numpy().tobytes() == ref_p[i].tobytes()
+        assert torch.equal(shadow[i], master[i].to(torch.bfloat16))
+
+
+def test_adamw_matches_torch_adamw():
+    """AdamW is pinned to torch.optim.AdamW(foreach=False) on CPU (no reference)."""
+    rng = np.random.default_rng(7)
+    th = rng.standard_normal(10007).astype(np.float32)
+    p = _param(th)
+    pol = of.OptimizerPolicy("adamw", eta=1e-3, weight_decay=0.05)
+    ref = torch.nn.Parameter(torch.from_numpy(th.copy()))
+    opt = torch.optim.AdamW([ref], lr=1e-3, weight_decay=0.05, foreach=False)
+    for s in range(20):
+        g = rng.standard_normal(10007).astype(np.float32)
+        pol.begin_iteration()
+        p.value.grad = torch.from_numpy(g.copy()).to(DEV)
+        pol.step(p)
+        ref.grad = torch.from_numpy(g.copy())
+        opt.step()
+    got = p.value.detach().cpu().numpy()
+    want = ref.detach().numpy()
+    rel = np.linalg.norm(got - want) / np.linalg.norm(want)
+    assert rel < 1e-6, rel
+    assert np.max(np.abs(got - want) / np.maximum(np.abs(want), 1e-3)) < 1e-5
+    st = opt.state[ref]
+    np.testing.assert_allclose(p.history["exp_avg"].cpu().numpy(), st["exp_avg"].numpy(),
+                               rtol=1e-5, atol=1e-9)
+    np.testing.assert_allclose(p.history["exp_avg_sq"].cpu().numpy(), st["exp_avg_sq"].numpy(),
+                               rtol=1e-5, atol=1e-12)
+
+
+def test_sqnorm_and_clip_factor():
+    rng = np.random.default_rng(11)
+    gs = [rng.standard_normal(int(k)).astype(np.float32) for k in (1, 7, 4096, 123457, 3)]
+    g = of.build_model("chain", layers=1, width=1, device=DEV)  # container for parameters
+    params = [_param(np.zeros_like(x), i) for i, x in enumerate(gs)]
+    for p, x in zip(params, gs):
+        p.value.grad = torch.from_numpy(x).to(DEV)
+    g.parameters = params
+    want_sq = sum(float(np.dot(x.astype(np.float64), x.astype(np.float64))) for x in gs)
+    norm = want_sq ** 0.5
+    f = of.clip_by_global_norm(g, 1.0)
+    assert abs(float(f) - 1.0 / norm) <= 1e-12 * (1.0 / norm)
+    assert params[0]._grad_scale is not None
+    assert float(of.clip_by_global_norm(g, 1e9)) == 1.0
+    # deterministic: same bits twice
+    a = float(of.clip_by_global_norm(g, 0.5))
+    b = float(of.clip_by_global_norm(g, 0.5))
+    assert a == b
+
+
+def test_spec_kats_on_gpu(spec_kats):
+    p = _param(np.array([1.0], np.float32))
+    p.value.grad = torch.tensor([2.0], device=DEV)
+    pol = of.OptimizerPolicy("sgd", eta=0.1)
+    pol.begin_iteration()
+    pol.step(p)
+    assert p.value.detach().cpu().tolist() == spec_kats["sgd"]["theta"]
+    assert p.value.grad.cpu().tolist() == [0.0]
+    p = _param(np.array([1.0], np.float32))
+    pol = of.OptimizerPolicy("sgd-momentum", eta=0.1, alpha=0.9)
+    got = []
+    for _ in range(2):
+        pol.begin_iteration()
+        p.value.grad = p.value.detach().clone()
+        pol.step(p)
+        got.append(float(p.value))
+    assert got == spec_kats["sgd_momentum"]["theta"]
+    p = _param(np.array([1.0], np.float32))
+    pol = of.OptimizerPolicy("sgd", eta=1.0, weight_decay=0.1)
+    pol.begin_iteration()
+    pol.step(p)
+    assert p.value.detach().cpu().tolist() == spec_kats["weight_decay"]["theta"]

@@ -1,0 +1,83 @@
+"""The C-ABI library loads and exports every symbol include/optfuse_b200.h
+declares; argument validation rejects bad calls before anything is launched
+(no GPU needed: nothing here reaches the CUDA runtime)."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+from paper_2104_00237_b200 import _native as nat
+from paper_2104_00237_b200 import kernels
+
+HEADER = Path(__file__).resolve().parent.parent / "include" / "optfuse_b200.h"
+
+
+def declared_symbols():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|uint64_t|const char\*)\s+(of_\w+)\(",
+                                 text, re.M)))
+
+
+def test_header_and_binding_agree():
+    assert declared_symbols() == sorted(nat.SYMBOLS)
+
+
+def test_library_exports_every_symbol():
+    so = nat.lib()
+    for name in declared_symbols():
+        assert hasattr(so, name), name
+    assert so.of_abi_version() == 1
+    assert so.of_status_string(0) == b"ok"
+    assert so.of_sqnorm_workspace_len() >= 148
+
+
+def test_library_is_sm100a_only():
+    data = nat.LIB_PATH.read_bytes()
+    assert b"sm_100a" in data
+
+
+def _hp(kind=1, eta=0.1):
+    return nat.OfHparams(kind, 0, eta, 0.9, 0.0, 1e-8, 0.9, 0.999, 0.9, 1.0, 1.0)
+
+
+def test_invalid_arguments_rejected_before_launch():
+    so = nat.lib()
+    before = so.of_launch_count()
+    hp = _hp()
+    assert so.of_policy_step_mt(None, ctypes.byref(hp), None, 0, None) == nat.OF_ERR_INVALID
+    assert b"NULL" in so.of_last_error()
+    tl = kernels.TensorList(1)
+    tl.param[0] = 0x1000
+    tl.grad[0] = None
+    tl.state0[0] = 0x2000
+    tl.numel[0] = 7
+    assert so.of_policy_step_mt(tl.ref, ctypes.byref(hp), None, 0, None) == nat.OF_ERR_INVALID
+    assert b"grad" in so.of_last_error()
+    bad = _hp(kind=42)
+    assert so.of_policy_step_mt(tl.ref, ctypes.byref(bad), None, 0, None) == nat.OF_ERR_INVALID
+    neg = _hp(eta=-1.0)
+    assert so.of_policy_step_mt(tl.ref, ctypes.byref(neg), None, 0, None) == nat.OF_ERR_INVALID
+    assert so.of_policy_step_mt(tl.ref, ctypes.byref(hp), None, 0x80, None) == nat.OF_ERR_INVALID
+    tl.struct.param_dtype = nat.OF_BF16
+    tl.grad[0] = 0x3000
+    assert so.of_policy_step_mt(tl.ref, ctypes.byref(hp), None, 0, None) == nat.OF_ERR_UNSUPPORTED
+    adam = nat.OfHparams(5, 0, 1e-3, 0.9, 0.0, 1e-8, 0.9, 0.999, 0.9, 0.0, 0.0)
+    tl.struct.param_dtype = nat.OF_F32
+    tl.state1[0] = 0x4000
+    assert so.of_policy_step_mt(tl.ref, ctypes.byref(adam), None, 0, None) == nat.OF_ERR_INVALID
+    assert b"bias" in so.of_last_error()
+    empty = kernels.TensorList(0)
+    assert so.of_policy_step_mt(empty.ref, ctypes.byref(hp), None, 0, None) == nat.OF_OK
+    assert so.of_clip_coef(None, 1.0, None, None, None) == nat.OF_ERR_INVALID
+    assert so.of_sqnorm_mt(empty.ref, None, 0, None, 0, None) == nat.OF_ERR_INVALID
+    assert so.of_launch_count() == before, "a rejected call must not launch"
+
+
+def test_check_raises_native_error():
+    from paper_2104_00237_b200.errors import NativeLibraryError
+    so = nat.lib()
+    so.of_policy_step_mt(None, None, None, 0, None)
+    with pytest.raises(NativeLibraryError, match="invalid"):
+        nat.check(nat.OF_ERR_INVALID, "of_policy_step_mt")
