@@ -57,6 +57,9 @@ def parse_args(argv=None):
                     choices=("baseline", "forward-fusion", "backward-fusion"))
     ap.add_argument("--workers", type=int, default=2, help="backward-fusion: 1 inline, >1 side stream")
     ap.add_argument("--grad-reset", default="none", choices=("zero", "none"))
+    ap.add_argument("--bucket-elems", type=int, default=0,
+                    help="backward-fusion launch groups: 0 = one per layer, else merge layers "
+                         "(backward order) into buckets of at least this many elements")
     ap.add_argument("--sweep", default="32,64,256,512", help="extra per-GPU batches ('' to skip)")
     ap.add_argument("--no-extras", action="store_true", help="headline only (for profilers)")
     ap.add_argument("--cpu-iters", type=int, default=2, help="CPU baseline sample iterations")
@@ -194,7 +197,7 @@ def load_peaks() -> dict:
 # ---------------------------------------------------------------------------
 
 def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
-                grad_reset=None, opt_impl=None):
+                grad_reset=None, opt_impl=None, bucket_elems=None):
     """Returns (step_fn, graph_or_model, policy_or_opt)."""
     import torch
     import torch.nn.functional as F
@@ -218,10 +221,11 @@ def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
         return step, net, opt
 
     g = of.build_classifier(args.model, device=device, seed=seed)
-    g.track_counts = True
+    g.track_counts = False  # no per-layer Python pre-hooks unless a schedule needs them
     pol = of.OptimizerPolicy("sgd-momentum", eta=0.1, alpha=0.9, weight_decay=5e-4,
                              grad_reset=grad_reset or args.grad_reset)
     w = args.workers if workers is None else workers
+    be = args.bucket_elems if bucket_elems is None else bucket_elems
     if schedule == "baseline":
         def step():
             of.run_baseline(g, pol, (x, y), timing=False)
@@ -230,7 +234,7 @@ def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
             of.run_forward_fusion(g, pol, (x, y), timing=False)
     else:
         def step():
-            of.run_backward_fusion(g, pol, (x, y), workers=w, timing=False)
+            of.run_backward_fusion(g, pol, (x, y), workers=w, timing=False, bucket_elems=be)
     return step, g, pol
 
 
@@ -275,27 +279,38 @@ def measure_update_kernel(args, device, peaks) -> dict:
     return out
 
 
-def measure_in_situ(args, device, peaks, steps: int) -> dict:
-    """Per-launch duration of the backward-fusion update kernel inside real
-    training iterations (events around each side-stream launch)."""
+def measure_in_situ(args, device, peaks, reps: int = 5) -> dict:
+    """Per-launch duration of the backward-fusion update kernel on its stream.
+
+    After real training iterations, the exact backward-fusion launch sequence
+    (same groups, tensors and hyper-parameters) is enqueued on the update
+    stream behind a torch.cuda._sleep, so the CUDA events around each launch
+    time the kernels back to back and never a host-side issue gap."""
     import torch
 
-    from paper_2104_00237_b200.optim import algorithmic_bytes
+    from paper_2104_00237_b200.optim import bytes_per_element
     step, g, pol = make_runner(args, args.batch, "backward-fusion", device, workers=2)
     for _ in range(3):
         step()
-    eng = g._bf_engine
-    eng.profile = []
-    for _ in range(steps):
+    eng = next(e for k, e in g._engines.items() if k[1])
+    native = eng.native
+    recs = []
+    for _ in range(reps):
         step()
-    torch.cuda.synchronize()
-    recs = eng.profile
-    eng.profile = None
-    tot_ms = sum(a.elapsed_time(b) for a, b, _ in recs)
-    tot_bytes = sum(algorithmic_bytes(pol.kind, ps) for _, _, ps in recs)
+        with torch.cuda.stream(eng.stream):
+            torch.cuda._sleep(20_000_000)
+        native.set_profile(True)
+        for gi in range(native.num_groups):
+            native.launch_group(gi)
+        native.set_profile(False)
+        native.join()
+        recs += native.take_profile()
+    bpe = bytes_per_element(pol.kind, 4)
+    tot_ms = sum(ms for ms, _ in recs)
+    tot_bytes = sum(n * bpe for _, n in recs)
     n = len(recs)
     gbs = tot_bytes / (tot_ms / 1e3) / 1e9
-    return {"launches_per_step": n // steps, "avg_bytes": tot_bytes / n, "avg_us": tot_ms / n * 1e3,
+    return {"launches_per_step": n // reps, "avg_bytes": tot_bytes / n, "avg_us": tot_ms / n * 1e3,
             "achieved_gbs": gbs, "frac": gbs / peaks["hbm_gbs"]}
 
 
@@ -339,27 +354,32 @@ def run_ours(args) -> dict:
            "config": {"workload": WORKLOAD, "model": args.model, "batch_per_gpu": args.batch,
                       "global_batch": args.batch * dist.world, "schedule": args.schedule,
                       "workers": args.workers, "grad_reset": args.grad_reset,
+                      "bucket_elems": args.bucket_elems,
                       "parallelism": f"dp{dist.world}",
                       "l2": "256 MiB buffer zeroed before every timed step (inside the timed region)"},
            "gpu_launches": launches}
     del step, g, pol
     if not args.no_extras:
         sched = {}
-        variants = [("torch.optim.SGD(foreach)", "baseline", None, None, "foreach"),
-                    ("torch.optim.SGD(fused)", "baseline", None, None, "fused"),
-                    ("ours:baseline", "baseline", None, None, None),
-                    ("ours:forward-fusion", "forward-fusion", None, None, None),
-                    ("ours:backward-fusion(w=1)", "backward-fusion", 1, None, None),
-                    ("ours:backward-fusion(w=2)", "backward-fusion", 2, None, None),
-                    ("ours:backward-fusion(w=2,zero)", "backward-fusion", 2, "zero", None)]
+        variants = [("torch.optim.SGD(foreach)", "baseline", None, None, "foreach", None),
+                    ("torch.optim.SGD(fused)", "baseline", None, None, "fused", None),
+                    ("ours:baseline", "baseline", None, None, None, None),
+                    ("ours:forward-fusion", "forward-fusion", None, None, None, None),
+                    ("ours:backward-fusion(w=1)", "backward-fusion", 1, None, None, 0),
+                    ("ours:backward-fusion(w=2)", "backward-fusion", 2, None, None, 0),
+                    ("ours:backward-fusion(w=2,zero)", "backward-fusion", 2, "zero", None, 0),
+                    ("ours:backward-fusion(w=1,bucket=256K)", "backward-fusion", 1, None, None, 1 << 18),
+                    ("ours:backward-fusion(w=2,bucket=256K)", "backward-fusion", 2, None, None, 1 << 18)]
         for b in [args.batch] + [int(s) for s in args.sweep.split(",") if s.strip()]:
             row = {}
-            for name, sch, w, gr, opt in variants:
+            for name, sch, w, gr, opt, be in variants:
                 if b != args.batch and name not in ("torch.optim.SGD(foreach)",
                                                     "ours:forward-fusion",
-                                                    "ours:backward-fusion(w=2)"):
+                                                    "ours:backward-fusion(w=2)",
+                                                    "ours:backward-fusion(w=1,bucket=256K)"):
                     continue
-                st, *_ = make_runner(args, b, sch, device, workers=w, grad_reset=gr, opt_impl=opt)
+                st, *_ = make_runner(args, b, sch, device, workers=w, grad_reset=gr, opt_impl=opt,
+                                     bucket_elems=be)
                 t = timed(st, args.steps, args.warmup, dist, flush)
                 row[name] = {"ms_per_step": round(t, 4), "images_per_s": round(b * 1e3 / t, 1)}
                 del st
@@ -369,9 +389,8 @@ def run_ours(args) -> dict:
                 v["speedup_vs_torch_foreach"] = round(base / v["ms_per_step"], 4)
             sched[str(b)] = row
         res["schedules"] = sched
-        res["speedup_vs_unfused_torch"] = sched[str(args.batch)][
-            f"ours:{args.schedule}" + ("(w=%d)" % args.workers if args.schedule == "backward-fusion" else "")
-        ]["speedup_vs_torch_foreach"] if args.schedule == "backward-fusion" else None
+        base_ms = sched[str(args.batch)]["torch.optim.SGD(foreach)"]["ms_per_step"]
+        res["speedup_vs_unfused_torch"] = round(base_ms / ms, 4)
         # end to end through the public API: pinned host batch -> device, loss -> host
         res["e2e"] = e2e(args, device, dist)
         ins = measure_in_situ(args, device, peaks, 5)
@@ -398,11 +417,13 @@ def e2e(args, device, dist) -> dict:
     xh, yh = synthetic_batch(args.model, args.batch, device="cpu")
     xh, yh = xh.pin_memory(), yh.pin_memory()
     g = of.build_classifier(args.model, device=device)
+    g.track_counts = False
     pol = of.OptimizerPolicy("sgd-momentum", eta=0.1, alpha=0.9, weight_decay=5e-4,
                              grad_reset=args.grad_reset)
     run = {"baseline": of.run_baseline, "forward-fusion": of.run_forward_fusion,
            "backward-fusion": of.run_backward_fusion}[args.schedule]
-    kw = {"workers": args.workers} if args.schedule == "backward-fusion" else {}
+    kw = ({"workers": args.workers, "bucket_elems": args.bucket_elems}
+          if args.schedule == "backward-fusion" else {})
 
     def step():
         x = xh.to(device, non_blocking=True)

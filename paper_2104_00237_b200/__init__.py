@@ -12,9 +12,10 @@ from .errors import (ConfigError, GlobalInfoRequired, NativeLibraryError, Numeri
                      SchedulingContractError, ShapeError, StateError)
 from .graph import Graph, Layer, Parameter
 from .models import build_classifier, build_model, iteration_inputs, make_input
+from .engine import FusionEngine, launch_groups
 from .optim import KINDS, OptimizerPolicy, clip_by_global_norm, newton_step
 from .schedule import (BACKWARD_FUSION, BASELINE, FORWARD_FUSION, SCHEDULES,
-                       BackwardFusionEngine, StepReport, check_inplace_safety,
+                       StepReport, check_inplace_safety,
                        flush_pending_updates, run_backward_fusion, run_baseline,
                        run_forward_fusion)
 from .trace import ScheduleTrace, critical_path_depth, validate_trace

@@ -44,8 +44,45 @@ def build_kernels(force: bool = False, verbose: bool = False) -> Path:
     return KERNEL_LIB
 
 
+ENGINE_SRC = PKG / "csrc" / "optfuse_engine.cpp"
+
+
+def engine_lib_path() -> Path:
+    import sysconfig
+    return PKG / ("_optfuse_engine" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
+def build_engine(force: bool = False, verbose: bool = False) -> Path:
+    """The native hook scheduler: a torch extension module linked against
+    liboptfuse_b200.so (found next to it through an $ORIGIN rpath)."""
+    import sysconfig
+
+    import torch
+    from torch.utils import cpp_extension as ce
+
+    target = engine_lib_path()
+    deps = [ENGINE_SRC, ROOT / "include" / "optfuse_b200.h", KERNEL_LIB]
+    if not force and not _stale(target, deps):
+        return target
+    incs = ce.include_paths("cuda") + [sysconfig.get_paths()["include"], str(ROOT / "include")]
+    libs = ce.library_paths("cuda")
+    abi = int(torch._C._GLIBCXX_USE_CXX11_ABI)
+    cmd = [os.environ.get("CXX", "g++"), "-O2", "-std=c++17", "-fPIC", "-shared",
+           f"-D_GLIBCXX_USE_CXX11_ABI={abi}", "-DTORCH_EXTENSION_NAME=_optfuse_engine",
+           "-DTORCH_API_INCLUDE_EXTENSION_H", "-fvisibility=hidden",
+           *[f"-I{i}" for i in incs], str(ENGINE_SRC), "-o", str(target),
+           *[f"-L{d}" for d in libs], f"-L{PKG}",
+           "-loptfuse_b200", "-lc10", "-lc10_cuda", "-ltorch", "-ltorch_cpu", "-ltorch_cuda",
+           "-ltorch_python", "-lcudart", "-Wl,-rpath,$ORIGIN"]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+    return target
+
+
 def build_all(force: bool = False, verbose: bool = False) -> None:
     build_kernels(force=force, verbose=verbose)
+    build_engine(force=force, verbose=verbose)
 
 
 if __name__ == "__main__":

@@ -1,0 +1,443 @@
+// optfuse_engine.cpp -- native hook scheduler for forward- and backward-fusion.
+//
+// The reference schedules updates from Python (schedule.py:98-207) and
+// overlaps them with backward through a Python thread pool (schedule.py:210-311).
+// On B200 the per-layer host work must cost well under the ~5-10 us a small
+// backward kernel takes, or the fused schedules become CPU-bound.  So the
+// whole per-layer path lives here, in C++:
+//
+//   * backward fusion: a C++ PostAccumulateGradHook on every parameter (fires
+//     once per iteration, after every contribution has been accumulated and
+//     after the consuming node computed its input gradient from the old value
+//     -- Appendix B.2's safety condition, schedule.py:54-59).  When the last
+//     parameter of a launch group (a layer, or a bucket of consecutive layers
+//     in backward order) is ready, the engine records an event on the
+//     autograd stream, makes the high-priority update stream wait on it and
+//     launches one multi-tensor update kernel there (liboptfuse_b200 C ABI).
+//     The compute stream joins the update stream once, at finish().
+//   * forward fusion: ff_layer(l), called from the layer's forward pre-hook,
+//     launches the update of every pending, not-yet-updated parameter of that
+//     layer on the compute stream right before the layer's kernels (the
+//     `updated` latch of schedule.py:112-121; the frozen step index of :133).
+//
+// Gradients are read straight from the parameters (param.grad()); with
+// release_grads the engine drops them after the launch (set-to-none), keeping
+// them alive in `hold_` until the update stream has been joined.
+#include <torch/extension.h>
+#include <ATen/cuda/CUDAContext.h>
+#include <torch/csrc/autograd/function_hook.h>
+#include <torch/csrc/autograd/variable.h>
+
+#include <cuda_runtime_api.h>
+
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "optfuse_b200.h"
+
+namespace {
+
+namespace py = pybind11;
+using torch::autograd::Variable;
+
+int dtype_code(at::ScalarType t) {
+  switch (t) {
+    case at::kFloat: return OF_F32;
+    case at::kDouble: return OF_F64;
+    case at::kBFloat16: return OF_BF16;
+    default: throw std::invalid_argument("optfuse: unsupported dtype for the update kernels");
+  }
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// A fixed list of parameters updated by one kernel launch.
+struct Group {
+  std::vector<int> members;
+  std::vector<void*> p, g, s0, s1, sh;
+  std::vector<int64_t> n;
+  of_tensor_list list{};
+  cudaEvent_t ready = nullptr;
+  int64_t elems = 0;
+
+  void bind() {
+    const size_t k = members.size();
+    p.resize(k); g.resize(k); s0.resize(k); s1.resize(k); sh.resize(k); n.resize(k);
+    list.n = static_cast<int32_t>(k);
+    list.param = p.data();
+    list.grad = g.data();
+    list.state0 = s0.data();
+    list.state1 = s1.data();
+    list.shadow = sh.data();
+    list.numel = n.data();
+  }
+};
+
+class Engine;
+
+struct FusionHook : torch::autograd::PostAccumulateGradHook {
+  std::weak_ptr<Engine> eng;
+  int idx;
+  FusionHook(std::weak_ptr<Engine> e, int i) : eng(std::move(e)), idx(i) {}
+  void operator()(const Variable& tensor) override;
+};
+
+class Engine : public std::enable_shared_from_this<Engine> {
+ public:
+  Engine(std::vector<at::Tensor> params, std::vector<std::vector<int>> bf_groups,
+         std::vector<std::vector<int>> layers, int64_t side_stream)
+      : params_(std::move(params)), layers_(std::move(layers)),
+        side_(reinterpret_cast<cudaStream_t>(side_stream)) {
+    const int np = static_cast<int>(params_.size());
+    s0_.assign(np, at::Tensor());
+    s1_.assign(np, at::Tensor());
+    group_of_.assign(np, -1);
+    pending_.assign(np, 0);
+    updated_.assign(np, 0);
+    for (auto& members : bf_groups) {
+      Group G;
+      G.members = members;
+      G.bind();
+      for (int idx : members) {
+        if (idx < 0 || idx >= np) throw std::out_of_range("optfuse: group member out of range");
+        if (group_of_[idx] != -1) throw std::invalid_argument("optfuse: parameter in two groups");
+        group_of_[idx] = static_cast<int>(groups_.size());
+        G.elems += params_[idx].numel();
+      }
+      if (side_) cuda_check(cudaEventCreateWithFlags(&G.ready, cudaEventDisableTiming), "cudaEventCreate");
+      groups_.push_back(std::move(G));
+    }
+    ready_.assign(groups_.size(), 0);
+    launched_.assign(groups_.size(), 0);
+    if (side_) cuda_check(cudaEventCreateWithFlags(&join_, cudaEventDisableTiming), "cudaEventCreate");
+    hp_ = of_hparams{};
+  }
+
+  ~Engine() {
+    remove_hooks();
+    for (auto& G : groups_)
+      if (G.ready) cudaEventDestroy(G.ready);
+    if (join_) cudaEventDestroy(join_);
+    clear_profile();
+  }
+
+  // -- configuration -------------------------------------------------------
+  void set_slots(int idx, c10::optional<at::Tensor> a, c10::optional<at::Tensor> b) {
+    s0_.at(idx) = a.has_value() ? *a : at::Tensor();
+    s1_.at(idx) = b.has_value() ? *b : at::Tensor();
+    // static pointers of the BF groups
+    const int gi = group_of_[idx];
+    if (gi >= 0) refresh_static(groups_[gi]);
+  }
+
+  void set_hparams(int kind, double eta, double alpha, double wd, double eps, double b1, double b2,
+                   double rho, double bc1, double bc2, int64_t flags, bool release_grads,
+                   c10::optional<at::Tensor> grad_scale) {
+    hp_.kind = kind;
+    hp_.eta = eta;
+    hp_.alpha = alpha;
+    hp_.weight_decay = wd;
+    hp_.epsilon = eps;
+    hp_.beta1 = b1;
+    hp_.beta2 = b2;
+    hp_.rho = rho;
+    hp_.bias_correction1 = bc1;
+    hp_.bias_correction2 = bc2;
+    flags_ = static_cast<uint32_t>(flags);
+    release_ = release_grads;
+    gscale_ = grad_scale.has_value() ? *grad_scale : at::Tensor();
+  }
+
+  // (Re)installs this engine's hook on every grouped parameter, replacing
+  // whatever post-accumulate-grad hook another engine of the graph had set.
+  void install_hooks() {
+    auto self = weak_from_this();
+    for (size_t i = 0; i < params_.size(); ++i) {
+      if (group_of_[i] < 0) continue;
+      torch::autograd::impl::set_post_acc_grad_hooks(
+          params_[i], std::make_unique<FusionHook>(self, static_cast<int>(i)));
+    }
+    hooks_installed_ = true;
+  }
+
+  void remove_hooks() {
+    if (!hooks_installed_) return;
+    for (auto& p : params_) {
+      auto& h = torch::autograd::impl::post_acc_grad_hooks(p);
+      auto* mine = h ? dynamic_cast<FusionHook*>(h.get()) : nullptr;
+      if (mine && mine->eng.lock().get() == this) torch::autograd::impl::set_post_acc_grad_hooks(p, nullptr);
+    }
+    hooks_installed_ = false;
+  }
+
+  void set_callback(py::object cb) { callback_ = cb.is_none() ? py::object() : cb; }
+
+  // -- backward fusion -----------------------------------------------------
+  // Arms the hooks for one backward pass.  launch=false only reports
+  // gradient readiness to the callback (schedule tracing of the unfused
+  // schedules).
+  void bf_begin(bool launch) {
+    std::fill(ready_.begin(), ready_.end(), 0);
+    std::fill(launched_.begin(), launched_.end(), 0);
+    armed_ = true;
+    launch_ = launch;
+  }
+
+  void disarm() { armed_ = false; }
+
+  void on_ready(int idx) {
+    if (!armed_) return;
+    if (callback_) {
+      py::gil_scoped_acquire gil;
+      callback_(idx);
+    }
+    const int gi = group_of_[idx];
+    if (gi < 0 || !launch_) return;
+    if (++ready_[gi] == static_cast<int>(groups_[gi].members.size())) launch_group(gi);
+  }
+
+  // Launch every group that did not complete during backward (parameters
+  // that received no gradient this iteration still step, with g = 0, as the
+  // reference steps every parameter), then join the update stream.
+  int bf_finish() {
+    armed_ = false;
+    int late = 0;
+    for (size_t gi = 0; gi < groups_.size(); ++gi) {
+      if (!launched_[gi]) {
+        launch_group(static_cast<int>(gi));
+        ++late;
+      }
+    }
+    join();
+    return late;
+  }
+
+  void join() {
+    if (side_) {
+      cuda_check(cudaEventRecord(join_, side_), "cudaEventRecord");
+      cuda_check(cudaStreamWaitEvent(current(), join_, 0), "cudaStreamWaitEvent");
+    }
+    hold_.clear();
+  }
+
+  // -- forward fusion ------------------------------------------------------
+  void set_all_pending() {
+    std::fill(pending_.begin(), pending_.end(), 1);
+    std::fill(updated_.begin(), updated_.end(), 0);
+  }
+  void clear_updated() { std::fill(updated_.begin(), updated_.end(), 0); }
+  bool is_pending(int idx) const { return pending_.at(idx) != 0; }
+  bool is_updated(int idx) const { return updated_.at(idx) != 0; }
+  void set_pending(int idx, bool v) { pending_.at(idx) = v; }
+  void set_updated(int idx, bool v) { updated_.at(idx) = v; }
+  int64_t num_pending() const {
+    int64_t c = 0;
+    for (auto v : pending_) c += v;
+    return c;
+  }
+
+  // Updates the pending, not yet updated parameters of layer `li` on the
+  // current stream; returns how many were updated.
+  int ff_layer(int li) {
+    const auto& lp = layers_.at(li);
+    scratch_.members.clear();
+    for (int idx : lp)
+      if (pending_[idx] && !updated_[idx]) scratch_.members.push_back(idx);
+    if (scratch_.members.empty()) return 0;
+    launch_dynamic(scratch_, current());
+    for (int idx : scratch_.members) {
+      updated_[idx] = 1;
+      pending_[idx] = 0;
+    }
+    return static_cast<int>(scratch_.members.size());
+  }
+
+  // Updates every pending parameter (layer order, each once) on the current
+  // stream: forward-fusion leftovers and flush_pending_updates.
+  int flush() {
+    scratch_.members.clear();
+    std::vector<uint8_t> seen(params_.size(), 0);
+    for (const auto& lp : layers_)
+      for (int idx : lp)
+        if (pending_[idx] && !seen[idx]) {
+          seen[idx] = 1;
+          scratch_.members.push_back(idx);
+        }
+    if (scratch_.members.empty()) return 0;
+    launch_dynamic(scratch_, current());
+    for (int idx : scratch_.members) pending_[idx] = 0;
+    return static_cast<int>(scratch_.members.size());
+  }
+
+  // -- profiling -----------------------------------------------------------
+  void set_profile(bool on) { profile_ = on; }
+  std::vector<std::pair<double, int64_t>> take_profile() {
+    std::vector<std::pair<double, int64_t>> out;
+    for (auto& r : prof_) {
+      cuda_check(cudaEventSynchronize(r.stop), "cudaEventSynchronize");
+      float ms = 0.f;
+      cuda_check(cudaEventElapsedTime(&ms, r.start, r.stop), "cudaEventElapsedTime");
+      out.emplace_back(ms, r.elems);
+    }
+    clear_profile();
+    return out;
+  }
+
+  // Launches group `gi` now (as its last gradient-ready hook would).
+  void launch_now(int gi) { launch_group(gi); }
+
+  int64_t launches() const { return launches_; }
+  int num_groups() const { return static_cast<int>(groups_.size()); }
+
+ private:
+  struct ProfRec {
+    cudaEvent_t start, stop;
+    int64_t elems;
+  };
+
+  static cudaStream_t current() { return at::cuda::getCurrentCUDAStream().stream(); }
+
+  void refresh_static(Group& G) {
+    for (size_t k = 0; k < G.members.size(); ++k) {
+      const int idx = G.members[k];
+      G.p[k] = params_[idx].data_ptr();
+      G.s0[k] = s0_[idx].defined() ? s0_[idx].data_ptr() : nullptr;
+      G.s1[k] = s1_[idx].defined() ? s1_[idx].data_ptr() : nullptr;
+      G.sh[k] = nullptr;
+      G.n[k] = params_[idx].numel();
+    }
+    G.list.param_dtype = dtype_code(params_[G.members[0]].scalar_type());
+  }
+
+  // Fills the grad pointers (allocating a zero gradient on the current stream
+  // where none exists).  Returns false if the group is empty.
+  void fill_grads(Group& G) {
+    for (size_t k = 0; k < G.members.size(); ++k) {
+      at::Tensor& gr = params_[G.members[k]].mutable_grad();
+      if (!gr.defined()) gr = at::zeros_like(params_[G.members[k]]);
+      G.g[k] = gr.data_ptr();
+      if (release_) hold_.push_back(gr);
+    }
+    G.list.grad_dtype = dtype_code(params_[G.members[0]].mutable_grad().scalar_type());
+  }
+
+  void release(const Group& G) {
+    if (!release_) return;
+    for (int idx : G.members) params_[idx].mutable_grad() = at::Tensor();
+  }
+
+  void launch(Group& G, cudaStream_t s) {
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (profile_) {
+      cuda_check(cudaEventCreate(&a), "cudaEventCreate");
+      cuda_check(cudaEventCreate(&b), "cudaEventCreate");
+      cuda_check(cudaEventRecord(a, s), "cudaEventRecord");
+    }
+    const float* gs = gscale_.defined() ? gscale_.data_ptr<float>() : nullptr;
+    const int st = of_policy_step_mt(&G.list, &hp_, gs, flags_, s);
+    if (st != OF_OK)
+      throw std::runtime_error(std::string("of_policy_step_mt: ") + of_status_string(st) + " (" +
+                               of_last_error() + ")");
+    if (profile_) {
+      cuda_check(cudaEventRecord(b, s), "cudaEventRecord");
+      prof_.push_back({a, b, G.elems});
+    }
+    ++launches_;
+  }
+
+  void launch_group(int gi) {
+    Group& G = groups_[gi];
+    fill_grads(G);
+    cudaStream_t cur = current();
+    cudaStream_t s = cur;
+    if (side_) {
+      cuda_check(cudaEventRecord(G.ready, cur), "cudaEventRecord");
+      cuda_check(cudaStreamWaitEvent(side_, G.ready, 0), "cudaStreamWaitEvent");
+      s = side_;
+    }
+    launch(G, s);
+    release(G);
+    launched_[gi] = 1;
+  }
+
+  void launch_dynamic(Group& G, cudaStream_t s) {
+    G.bind();
+    G.elems = 0;
+    for (int idx : G.members) G.elems += params_[idx].numel();
+    refresh_static(G);
+    fill_grads(G);
+    launch(G, s);
+    release(G);
+    if (release_) hold_.clear();  // same-stream use: the allocator orders reuse after it
+  }
+
+  void clear_profile() {
+    for (auto& r : prof_) {
+      cudaEventDestroy(r.start);
+      cudaEventDestroy(r.stop);
+    }
+    prof_.clear();
+  }
+
+  std::vector<at::Tensor> params_, s0_, s1_;
+  std::vector<std::vector<int>> layers_;
+  std::vector<Group> groups_;
+  Group scratch_;
+  std::vector<int> group_of_, ready_;
+  std::vector<uint8_t> launched_, pending_, updated_;
+  std::vector<at::Tensor> hold_;
+  of_hparams hp_;
+  uint32_t flags_ = 0;
+  bool release_ = false;
+  at::Tensor gscale_;
+  cudaStream_t side_ = nullptr;
+  cudaEvent_t join_ = nullptr;
+  bool armed_ = false;
+  bool launch_ = true;
+  bool hooks_installed_ = false;
+  bool profile_ = false;
+  std::vector<ProfRec> prof_;
+  int64_t launches_ = 0;
+  py::object callback_;
+};
+
+void FusionHook::operator()(const Variable&) {
+  if (auto e = eng.lock()) e->on_ready(idx);
+}
+
+}  // namespace
+
+PYBIND11_MODULE(_optfuse_engine, m) {
+  m.doc() = "Native hook scheduler for forward/backward fusion (liboptfuse_b200 launches)";
+  py::class_<Engine, std::shared_ptr<Engine>>(m, "Engine")
+      .def(py::init<std::vector<at::Tensor>, std::vector<std::vector<int>>,
+                    std::vector<std::vector<int>>, int64_t>(),
+           py::arg("params"), py::arg("bf_groups"), py::arg("layers"), py::arg("side_stream"))
+      .def("set_slots", &Engine::set_slots)
+      .def("set_hparams", &Engine::set_hparams)
+      .def("install_hooks", &Engine::install_hooks)
+      .def("remove_hooks", &Engine::remove_hooks)
+      .def("set_callback", &Engine::set_callback)
+      .def("bf_begin", &Engine::bf_begin, py::arg("launch") = true)
+      .def("disarm", &Engine::disarm)
+      .def("bf_finish", &Engine::bf_finish)
+      .def("join", &Engine::join)
+      .def("set_all_pending", &Engine::set_all_pending)
+      .def("clear_updated", &Engine::clear_updated)
+      .def("is_pending", &Engine::is_pending)
+      .def("is_updated", &Engine::is_updated)
+      .def("set_pending", &Engine::set_pending)
+      .def("set_updated", &Engine::set_updated)
+      .def("num_pending", &Engine::num_pending)
+      .def("ff_layer", &Engine::ff_layer)
+      .def("flush", &Engine::flush)
+      .def("set_profile", &Engine::set_profile)
+      .def("take_profile", &Engine::take_profile)
+      .def("launch_group", &Engine::launch_now)
+      .def_property_readonly("launches", &Engine::launches)
+      .def_property_readonly("num_groups", &Engine::num_groups);
+}

@@ -11,11 +11,12 @@ exactly the reference's per-parameter scheduling state and its two hook sites:
 * the forward hook site (graph.py:171-218): a forward pre-hook on every layer
   -- a module owning parameters directly -- that increments ``count`` and
   runs the schedule's ``pre_node_hook`` *before* the layer executes;
-* the gradient-ready site (graph.py:85-131): ``register_post_accumulate_grad_hook``
-  on every parameter.  AccumulateGrad fires it once, after every use of the
-  parameter has contributed (shared/tied parameters included) and after the
-  consuming node computed its input gradient from the old value, which is
-  Appendix B.2's in-place safety condition (schedule.py:54-59) on the host.
+* the gradient-ready site (graph.py:85-131): a C++ PostAccumulateGradHook on
+  every parameter, installed by the native engine (engine.py).  AccumulateGrad
+  fires it once, after every use of the parameter has contributed
+  (shared/tied parameters included) and after the consuming node computed its
+  input gradient from the old value, which is Appendix B.2's in-place safety
+  condition (schedule.py:54-59) on the host.
 
 A layer is a module with direct parameters; a parameter shared by several
 layers (tied embeddings, ``shared-chain``) is one ``Parameter`` bound to each.
@@ -30,10 +31,14 @@ from .errors import StateError
 
 
 class Parameter:
-    """A trainable tensor plus its scheduling state (graph.py:27-45)."""
+    """A trainable tensor plus its scheduling state (graph.py:27-45).
 
-    __slots__ = ("id", "name", "value", "history", "count", "updated", "pending",
-                 "_grad_scale", "_layout_ok", "layers")
+    While a native fusion engine owns the forward-fusion flags of the graph,
+    ``pending`` and ``updated`` read and write them there.
+    """
+
+    __slots__ = ("id", "name", "value", "history", "count", "_updated", "_pending",
+                 "_grad_scale", "_layout_ok", "layers", "_flags")
 
     def __init__(self, pid: int, value: torch.Tensor, name: str = ""):
         self.id = pid
@@ -41,11 +46,38 @@ class Parameter:
         self.value = value
         self.history: dict = {}
         self.count = 0
-        self.updated = False
-        self.pending = False
+        self._updated = False
+        self._pending = False
         self._grad_scale = None
         self._layout_ok = False
         self.layers: list = []
+        self._flags = None
+
+    @property
+    def pending(self) -> bool:
+        f = self._flags
+        return self._pending if f is None else f.is_pending(self.id)
+
+    @pending.setter
+    def pending(self, v: bool) -> None:
+        f = self._flags
+        if f is None:
+            self._pending = bool(v)
+        else:
+            f.set_pending(self.id, bool(v))
+
+    @property
+    def updated(self) -> bool:
+        f = self._flags
+        return self._updated if f is None else f.is_updated(self.id)
+
+    @updated.setter
+    def updated(self, v: bool) -> None:
+        f = self._flags
+        if f is None:
+            self._updated = bool(v)
+        else:
+            f.set_updated(self.id, bool(v))
 
     @property
     def grad(self):
@@ -109,18 +141,18 @@ class Graph:
         self._by_tensor = by_tensor
         # per-iteration state
         self.pending_step_t = None
+        self.pending_scale = None     # clip factor riding with the deferred updates
         self._forward_done = False
         self._loss = None
         self._input = None
         self._trace = None
         self._pre_node_hook = None
         self._prev_fwd_task = None
-        self._ff_hook = None          # forward-fusion apply_pending(layer), set by the schedule
-        self._grad_ready = None       # backward-fusion callback(param), set by the schedule
-        self._acc_handles = None
-        self._bf_engine = None
-        self._pre_handles = [layer.module.register_forward_pre_hook(self._make_pre_hook(layer))
-                             for layer in self.layers]
+        self._ff_hook = None          # forward-fusion apply(layer), set by the schedule
+        self._engines: dict = {}      # native fusion engines, by configuration
+        self._flag_owner = None       # engine holding the pending/updated flags
+        self._hook_owner = None       # engine whose C++ hooks sit on the parameters
+        self._pre_handles = None
 
     # -- structure ---------------------------------------------------------
 
@@ -162,24 +194,33 @@ class Graph:
             return None
         return pre_hook
 
-    def install_grad_ready_hooks(self) -> None:
-        """Register the post-accumulate-grad hook on every parameter (once)."""
-        if self._acc_handles is not None:
-            return
-        handles = []
-        for p in self.parameters:
-            def hook(tensor, p=p):
-                cb = self._grad_ready
-                if cb is not None:
-                    cb(p)
-            handles.append(p.value.register_post_accumulate_grad_hook(hook))
-        self._acc_handles = handles
-
-    def remove_grad_ready_hooks(self) -> None:
-        if self._acc_handles is not None:
-            for h in self._acc_handles:
+    def _sync_pre_hooks(self, needed: bool) -> None:
+        """Forward pre-hooks cost host time on every layer call, so they are
+        installed only while something uses them (counts, forward fusion, a
+        pre_node_hook or a trace)."""
+        if needed and self._pre_handles is None:
+            self._pre_handles = [L.module.register_forward_pre_hook(self._make_pre_hook(L))
+                                 for L in self.layers]
+        elif not needed and self._pre_handles is not None:
+            for h in self._pre_handles:
                 h.remove()
-            self._acc_handles = None
+            self._pre_handles = None
+
+    def set_flag_owner(self, eng) -> None:
+        """Move the forward-fusion flags into ``eng`` (a native engine) or back
+        to the Parameter objects (``eng=None``)."""
+        old = self._flag_owner
+        if old is eng:
+            return
+        state = [(p.pending, p.updated) for p in self.parameters]
+        for p, (pend, upd) in zip(self.parameters, state):
+            p._flags = None
+            p._pending, p._updated = pend, upd
+            if eng is not None:
+                eng.set_pending(p.id, pend)
+                eng.set_updated(p.id, upd)
+                p._flags = eng
+        self._flag_owner = eng
 
     # -- execution -----------------------------------------------------------
 
@@ -195,6 +236,8 @@ class Graph:
         self._trace = trace
         self._pre_node_hook = pre_node_hook
         self._prev_fwd_task = None
+        self._sync_pre_hooks(self.track_counts or self._ff_hook is not None
+                             or pre_node_hook is not None or trace is not None)
         if isinstance(inp, (tuple, list)):
             x, target = inp[0], inp[1]
         else:

@@ -184,16 +184,21 @@ class OptimizerPolicy:
         zero history slots on first use (optim.py:90-94) and a zero gradient
         for a parameter that received no contribution this iteration (the
         reference steps every parameter, with g = 0, schedule.py:87)."""
-        slots = _HISTORY_SLOTS[self.kind]
         for p in params:
             v = p.value
             if v.grad is None:
                 v.grad = torch.zeros_like(v)
+        self.prepare_history(params)
+
+    def prepare_history(self, params) -> None:
+        """Zero history slots on first use (optim.py:90-94)."""
+        slots = _HISTORY_SLOTS[self.kind]
+        for p in params:
             h = p.history
             if len(h) < len(slots):
                 for name in slots:
                     if name not in h:
-                        h[name] = torch.zeros_like(v, memory_format=torch.preserve_format)
+                        h[name] = torch.zeros_like(p.value, memory_format=torch.preserve_format)
 
     def _hparams(self, t: int) -> nat.OfHparams:
         key = (t, self.kind, self.eta, self.alpha, self.weight_decay, self.epsilon,
@@ -244,6 +249,39 @@ def _check_layout(p, g) -> None:
     p._layout_ok = True
 
 
+def clip_factor(graph, max_norm: float, trace: tr.ScheduleTrace | None = None, stream=None):
+    """Device half of the global-norm clip: returns (factor, coef), a 0-dim
+    float64 factor (optim.py:165-168) and its float32 multiplier."""
+    params = graph.parameters
+    dev = params[0].value.device
+    sq = torch.empty((), dtype=torch.float64, device=dev)
+    factor = torch.empty((), dtype=torch.float64, device=dev)
+    coef = torch.empty((), dtype=torch.float32, device=dev)
+    ws = torch.empty(kernels.sqnorm_workspace_len(), dtype=torch.float64, device=dev)
+    by_dtype: dict = {}
+    for p in params:
+        if trace is not None:
+            trace.record_mem(tr.GRAD, p.id, tr.READ)
+        g = p.value.grad
+        if g is not None:
+            by_dtype.setdefault(g.dtype, []).append(g)
+    if not by_dtype:
+        sq.zero_()
+    first = True
+    for dt, gl in by_dtype.items():
+        tl = kernels.TensorList(len(gl))
+        for i, g in enumerate(gl):
+            tl.set(i, None, g)
+        tl.set_dtypes(dt if dt != torch.bfloat16 else torch.float32, dt)
+        kernels.sqnorm(tl, ws, sq, accumulate=not first, stream=stream)
+        first = False
+    kernels.clip_coef(sq, max_norm, coef, factor, stream)
+    if trace is not None:
+        for p in params:
+            trace.record_mem(tr.GRAD, p.id, tr.WRITE)
+    return factor, coef
+
+
 def clip_by_global_norm(graph, max_norm: float, trace: tr.ScheduleTrace | None = None,
                         stream=None) -> torch.Tensor:
     """Global-norm clip (optim.py:151-172) as a device reduction.
@@ -254,35 +292,9 @@ def clip_by_global_norm(graph, max_norm: float, trace: tr.ScheduleTrace | None =
     its next update -- the reference's in-place ``grad *= factor`` without a
     second pass over the gradients.
     """
-    params = graph.parameters
-    grads = [p.value.grad for p in params]
-    live = [g for g in grads if g is not None]
-    dev = params[0].value.device
-    sq = torch.empty((), dtype=torch.float64, device=dev)
-    factor = torch.empty((), dtype=torch.float64, device=dev)
-    coef = torch.empty((), dtype=torch.float32, device=dev)
-    ws = torch.empty(kernels.sqnorm_workspace_len(), dtype=torch.float64, device=dev)
-    if trace is not None:
-        for p in params:
-            trace.record_mem(tr.GRAD, p.id, tr.READ)
-    first = True
-    by_dtype: dict = {}
-    for g in live:
-        by_dtype.setdefault(g.dtype, []).append(g)
-    if not by_dtype:
-        sq.zero_()
-    for dt, gl in by_dtype.items():
-        tl = kernels.TensorList(len(gl))
-        for i, g in enumerate(gl):
-            tl.set(i, None, g)
-        tl.set_dtypes(dt if dt != torch.bfloat16 else torch.float32, dt)
-        kernels.sqnorm(tl, ws, sq, accumulate=not first, stream=stream)
-        first = False
-    kernels.clip_coef(sq, max_norm, coef, factor, stream)
-    for p in params:
+    factor, coef = clip_factor(graph, max_norm, trace, stream)
+    for p in graph.parameters:
         p._grad_scale = coef
-        if trace is not None:
-            trace.record_mem(tr.GRAD, p.id, tr.WRITE)
     return factor
 
 

@@ -32,7 +32,7 @@ import torch
 from . import trace as tr
 from .errors import ConfigError, GlobalInfoRequired
 from .graph import Graph, Parameter
-from .optim import OptimizerPolicy, clip_by_global_norm
+from .optim import OptimizerPolicy, clip_by_global_norm, clip_factor
 
 BASELINE = "baseline"
 FORWARD_FUSION = "forward-fusion"
@@ -110,33 +110,86 @@ class _Marks:
             self.events.append(ev)
 
 
-class _TraceHooks:
-    """Records backward-node tasks (and nothing else) when a trace is on."""
+class _TraceRecorder:
+    """Host-side schedule trace from the engine's gradient-ready callback:
+    records the backward node(s) a ready parameter completes and, for backward
+    fusion, the step task of each launch group once all its members are ready
+    (the same counting the native engine does)."""
 
-    def __init__(self, graph: Graph, trace: tr.ScheduleTrace):
+    def __init__(self, graph: Graph, trace: tr.ScheduleTrace, groups=None):
         self.graph = graph
         self.trace = trace
         self.done: set = set()
         self.prev = trace.tasks[-1].task_id if trace.tasks else None
         self.last_of: dict = {}
+        self.groups = groups
+        if groups is not None:
+            self.group_of = {pid: gi for gi, g in enumerate(groups) for pid in g}
+            self.ready = [0] * len(groups)
+            self.stepped = [False] * len(groups)
 
-    def backward_nodes_for(self, p: Parameter) -> list:
-        """Record the backward node of every layer binding ``p`` not yet
-        recorded (reverse layer order); returns the task ids."""
-        ids = []
+    def backward_nodes_for(self, p: Parameter) -> None:
         for layer in sorted(p.layers, key=lambda L: -L.index):
             if layer.index in self.done:
                 continue
             self.done.add(layer.index)
             deps = () if self.prev is None else (self.prev,)
             self.prev = self.trace.add_task(tr.BACKWARD, layer.index, deps)
-            ids.append(self.prev)
-        if ids:
-            self.last_of[p.id] = ids[-1]
-        return ids
+            self.last_of[p.id] = self.prev
 
-    def __call__(self, p: Parameter) -> None:
+    def steps_for_group(self, gi: int) -> None:
+        self.stepped[gi] = True
+        for pid in self.groups[gi]:
+            dep = self.last_of.get(pid)
+            self.trace.add_task(tr.OPT_STEP, pid, () if dep is None else (dep,))
+
+    def __call__(self, pid: int) -> None:
+        p = self.graph.parameters[pid]
+        p.count = 0
         self.backward_nodes_for(p)
+        if self.groups is not None:
+            gi = self.group_of[pid]
+            self.ready[gi] += 1
+            if self.ready[gi] == len(self.groups[gi]):
+                self.steps_for_group(gi)
+
+    def finish(self) -> None:
+        if self.groups is not None:
+            for gi, done in enumerate(self.stepped):
+                if not done:
+                    self.steps_for_group(gi)
+
+
+def _engine(graph: Graph, policy: OptimizerPolicy, side: bool, bucket_elems: int = 0):
+    from .engine import FusionEngine
+    key = (policy.kind, side, bucket_elems)
+    eng = graph._engines.get(key)
+    if eng is None:
+        eng = FusionEngine(graph, policy, side, bucket_elems)
+        graph._engines[key] = eng
+    return eng
+
+
+def _own_hooks(graph: Graph, eng) -> None:
+    """One post-accumulate-grad hook slot per tensor: make ``eng`` its owner."""
+    if graph._hook_owner is not eng:
+        eng.native.install_hooks()
+        graph._hook_owner = eng
+
+
+def _traced_backward(graph: Graph, policy: OptimizerPolicy, tc) -> None:
+    """Backward of an unfused schedule with the engine hooks reporting
+    gradient readiness (no launches) to the trace recorder."""
+    eng = _engine(graph, policy, False)
+    rec = _TraceRecorder(graph, tc)
+    _own_hooks(graph, eng)
+    eng.native.set_callback(rec)
+    eng.native.bf_begin(False)
+    try:
+        graph.backward(tc)
+    finally:
+        eng.native.disarm()
+        eng.native.set_callback(None)
 
 
 def run_baseline(graph: Graph, policy: OptimizerPolicy, inp, *, timing: bool = True,
@@ -150,12 +203,9 @@ def run_baseline(graph: Graph, policy: OptimizerPolicy, inp, *, timing: bool = T
     loss = graph.forward(inp, tc)
     marks.mark()
     if tc is not None:
-        graph.install_grad_ready_hooks()
-        graph._grad_ready = _TraceHooks(graph, tc)
-    try:
-        graph.backward(tc)
-    finally:
-        graph._grad_ready = None
+        _traced_backward(graph, policy, tc)
+    else:
+        graph.backward()
     marks.mark()
     prev = tc.tasks[-1].task_id if tc is not None and tc.tasks else None
     if policy.clip_norm is not None:
@@ -175,27 +225,33 @@ def run_forward_fusion(graph: Graph, policy: OptimizerPolicy, inp, *, timing: bo
                        trace: bool = False) -> StepReport:
     """Lazy schedule: deferred updates applied just before each layer's forward.
 
-    The ``updated`` latch applies a shared parameter once; new gradients are
-    deferred at the end of backward, tagged with this iteration's step index
-    (schedule.py:130-133).  Global-information transforms are legal: the clip
-    factor is computed once all gradients exist and rides along with the
-    deferred updates.
+    The layer's forward pre-hook calls the native engine, which launches the
+    update of that layer's pending, not yet ``updated`` parameters on the
+    compute stream (the latch applies a shared parameter once); new gradients
+    are deferred at the end of backward, tagged with this iteration's step
+    index (schedule.py:130-133).  Global-information transforms are legal: the
+    clip factor is computed once all gradients exist and rides along with the
+    deferred updates as a device scalar.
     """
     _reject_newton(policy)
+    eng = _engine(graph, policy, False)
+    graph.set_flag_owner(eng.native)
     policy.begin_iteration()
     tc = tr.ScheduleTrace(FORWARD_FUSION) if trace else None
-    step_t = graph.pending_step_t
+    if graph.pending_step_t is not None:
+        eng.configure(policy, graph.pending_step_t, graph.pending_scale)
+    native = eng.native
+    ff_layer = native.ff_layer
 
-    def apply_pending(layer):
-        todo = [p for p in layer.params if p.pending and not p.updated]
-        if not todo:
+    if tc is None:
+        def apply_pending(layer):
+            ff_layer(layer.index)
             return None
-        policy.step_params(todo, step_t=step_t, trace=tc)
-        for p in todo:
-            p.updated = True
-        if tc is None:
-            return None
-        return [tc.add_task(tr.OPT_STEP, p.id, ()) for p in todo]
+    else:
+        def apply_pending(layer):
+            todo = [p.id for p in layer.params if p.pending and not p.updated]
+            ff_layer(layer.index)
+            return [tc.add_task(tr.OPT_STEP, pid, ()) for pid in todo]
 
     marks = _Marks(timing)
     marks.mark()
@@ -206,25 +262,21 @@ def run_forward_fusion(graph: Graph, policy: OptimizerPolicy, inp, *, timing: bo
         graph._ff_hook = None
     # a pending parameter whose layer did not run this forward is applied now,
     # before this iteration's gradients accumulate on top of its old ones
-    leftover = [p for p in graph.parameters if p.pending]
-    if leftover:
-        policy.step_params(leftover, step_t=step_t, trace=tc)
+    if native.num_pending():
+        native.flush()
     marks.mark()
     if tc is not None:
-        graph.install_grad_ready_hooks()
-        graph._grad_ready = _TraceHooks(graph, tc)
-    try:
-        graph.backward(tc)
-    finally:
-        graph._grad_ready = None
+        _traced_backward(graph, policy, tc)
+    else:
+        graph.backward()
+    scale = None
     if policy.clip_norm is not None:
-        clip_by_global_norm(graph, policy.clip_norm, tc)
+        scale = clip_factor(graph, policy.clip_norm, tc)[1]
         if tc is not None:
             tc.add_task(tr.CLIP_BARRIER, -1, (tc.tasks[-1].task_id,))
-    for p in graph.parameters:
-        p.pending = True
-        p.updated = False
+    native.set_all_pending()
     graph.pending_step_t = policy.t
+    graph.pending_scale = scale
     marks.mark()
     marks.mark()
     return StepReport(FORWARD_FUSION, loss, tc, marks.events, fused=True,
@@ -236,6 +288,7 @@ def flush_pending_updates(graph: Graph, policy: OptimizerPolicy,
     """Apply every deferred update as the next forward pass would (layer order,
     frozen step index); idempotent (schedule.py:141-160).  Must precede any
     observation of parameter values (eval, state_dict, checkpoint)."""
+    owner = graph._flag_owner
     todo = []
     seen: set = set()
     for layer in graph.layers:
@@ -245,110 +298,30 @@ def flush_pending_updates(graph: Graph, policy: OptimizerPolicy,
                 todo.append(p)
     if not todo:
         return 0
-    policy.step_params(todo, step_t=graph.pending_step_t, trace=trace)
+    if owner is not None:
+        eng = _engine(graph, policy, False)
+        eng.configure(policy, graph.pending_step_t, graph.pending_scale)
+        n = eng.native.flush()
+    else:
+        policy.step_params(todo, step_t=graph.pending_step_t)
+        n = len(todo)
     if trace is not None:
         prev = None
         for p in todo:
             prev = trace.add_task(tr.FLUSH, p.id, () if prev is None else (prev,))
-    return len(todo)
-
-
-class BackwardFusionEngine:
-    """Per-graph state of backward fusion: launch groups, readiness counters,
-    the update side stream and its events (the GPU ``_ParallelRunner``).
-
-    Launch groups are layers: each parameter belongs to the first layer that
-    binds it, so a shared parameter is updated once, after its last use (its
-    AccumulateGrad fires once, after all contributions).
-    """
-
-    def __init__(self, graph: Graph, side_stream: bool):
-        self.graph = graph
-        groups, seen = [], set()
-        for layer in graph.layers:
-            ps = [p for p in layer.params if p.id not in seen]
-            seen.update(p.id for p in ps)
-            if ps:
-                groups.append(ps)
-        self.groups = groups
-        self.group_of = {}
-        for gi, ps in enumerate(groups):
-            for p in ps:
-                self.group_of[p.id] = gi
-        self.size = [len(g) for g in groups]
-        self.ready = [0] * len(groups)
-        self.launched = [False] * len(groups)
-        self.stream = torch.cuda.Stream(priority=-1) if side_stream else None
-        self.events = [torch.cuda.Event() for _ in groups] if side_stream else None
-        self.join = torch.cuda.Event() if side_stream else None
-        self.hold: list = []
-        self.policy = None
-        self.trace_hooks = None
-        # optional instrumentation: (start event, end event, params) per
-        # side-stream launch, for the bench's in-situ kernel timing
-        self.profile = None
-
-    def begin(self, policy: OptimizerPolicy, tc) -> None:
-        self.policy = policy
-        self.ready = [0] * len(self.groups)
-        self.launched = [False] * len(self.groups)
-        self.trace_hooks = _TraceHooks(self.graph, tc) if tc is not None else None
-
-    def on_grad_ready(self, p: Parameter) -> None:
-        p.count = 0
-        if self.trace_hooks is not None:
-            self.trace_hooks.backward_nodes_for(p)
-        gi = self.group_of[p.id]
-        self.ready[gi] += 1
-        if self.ready[gi] == self.size[gi]:
-            self._launch(gi)
-
-    def _launch(self, gi: int) -> None:
-        params = self.groups[gi]
-        policy = self.policy
-        tc = self.trace_hooks.trace if self.trace_hooks is not None else None
-        if self.stream is None:
-            policy.step_params(params, trace=tc)
-        else:
-            policy.prepare(params, hold=self.hold)
-            ev = self.events[gi]
-            ev.record(torch.cuda.current_stream())
-            self.stream.wait_event(ev)
-            if self.profile is not None:
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(self.stream)
-                policy.step_params(params, trace=tc, stream=self.stream, hold=self.hold)
-                e1.record(self.stream)
-                self.profile.append((e0, e1, params))
-            else:
-                policy.step_params(params, trace=tc, stream=self.stream, hold=self.hold)
-        self.launched[gi] = True
-        if tc is not None:
-            for p in params:
-                dep = self.trace_hooks.last_of.get(p.id)
-                tc.add_task(tr.OPT_STEP, p.id, () if dep is None else (dep,))
-
-    def finish(self) -> None:
-        # groups that did not complete during backward (parameters that got no
-        # gradient this iteration): the reference still steps them with g = 0
-        for gi, done in enumerate(self.launched):
-            if not done:
-                for p in self.groups[gi]:
-                    p.count = 0
-                self._launch(gi)
-        if self.stream is not None:
-            self.join.record(self.stream)
-            torch.cuda.current_stream().wait_event(self.join)
-        self.hold.clear()
-        self.policy = None
-        self.trace_hooks = None
+    return n
 
 
 def run_backward_fusion(graph: Graph, policy: OptimizerPolicy, inp, workers: int = 1, *,
-                        timing: bool = True, trace: bool = False) -> StepReport:
+                        timing: bool = True, trace: bool = False,
+                        bucket_elems: int = 0) -> StepReport:
     """Eager schedule: update each layer as soon as its gradients are complete.
 
+    ``workers=1`` issues each update inline on the autograd stream;
+    ``workers>1`` on the engine's high-priority side stream behind an event
+    (the device half of the Appendix B.2 guard), overlapping the backward of
+    the preceding layers.  ``bucket_elems`` merges consecutive layers (backward
+    order) into launch groups of at least that many elements.
     Raises GlobalInfoRequired, mutating nothing, for policies or transforms
     that must see all gradients first (schedule.py:174-177).
     """
@@ -359,25 +332,32 @@ def run_backward_fusion(graph: Graph, policy: OptimizerPolicy, inp, workers: int
     _reject_newton(policy)
     if workers < 1:
         raise ConfigError(f"workers must be >= 1, got {workers}")
-    side = workers > 1
-    eng = graph._bf_engine
-    if eng is None or (eng.stream is not None) != side:
-        eng = BackwardFusionEngine(graph, side)
-        graph._bf_engine = eng
+    if bucket_elems < 0:
+        raise ConfigError(f"bucket_elems must be >= 0, got {bucket_elems}")
+    eng = _engine(graph, policy, workers > 1, bucket_elems)
     policy.begin_iteration()
+    eng.configure(policy, policy.t, None)
     tc = tr.ScheduleTrace(BACKWARD_FUSION) if trace else None
     marks = _Marks(timing)
     marks.mark()
     loss = graph.forward(inp, tc)
     marks.mark()
-    graph.install_grad_ready_hooks()
-    eng.begin(policy, tc)
-    graph._grad_ready = eng.on_grad_ready
+    native = eng.native
+    _own_hooks(graph, eng)
+    rec = None
+    if tc is not None:
+        rec = _TraceRecorder(graph, tc, eng.groups)
+        native.set_callback(rec)
+    native.bf_begin(True)
     try:
         graph.backward(tc)
-        eng.finish()
     finally:
-        graph._grad_ready = None
+        native.disarm()
+        if rec is not None:
+            native.set_callback(None)
+    native.bf_finish()
+    if rec is not None:
+        rec.finish()
     marks.mark()
     marks.mark()
     return StepReport(BACKWARD_FUSION, loss, tc, marks.events, fused=True)
