@@ -56,8 +56,10 @@ def parse_args(argv=None):
     ap.add_argument("--schedule", default="backward-fusion",
                     choices=("baseline", "forward-fusion", "backward-fusion"))
     ap.add_argument("--workers", type=int, default=2, help="backward-fusion: 1 inline, >1 side stream")
+    ap.add_argument("--ff-bucket-elems", type=int, default=1 << 18,
+                    help="forward-fusion buckets (0 = one pre-hook per layer)")
     ap.add_argument("--grad-reset", default="none", choices=("zero", "none"))
-    ap.add_argument("--bucket-elems", type=int, default=0,
+    ap.add_argument("--bucket-elems", type=int, default=1 << 18,
                     help="backward-fusion launch groups: 0 = one per layer, else merge layers "
                          "(backward order) into buckets of at least this many elements")
     ap.add_argument("--sweep", default="32,64,256,512", help="extra per-GPU batches ('' to skip)")
@@ -208,9 +210,7 @@ def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
     x, y = synthetic_batch(args.model, batch, device=device, seed=seed)
     if opt_impl is not None:  # unfused torch.optim baseline
         g = of.build_classifier(args.model, device=device, seed=seed)
-        net = g.module
-        for h in g._pre_handles:
-            h.remove()
+        net = g.module  # plain module: the Graph installs no hooks until a schedule runs
         kw = {"foreach": True} if opt_impl == "foreach" else {"fused": True}
         opt = torch.optim.SGD(net.parameters(), lr=0.1, momentum=0.9, weight_decay=5e-4, **kw)
 
@@ -230,8 +230,10 @@ def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
         def step():
             of.run_baseline(g, pol, (x, y), timing=False)
     elif schedule == "forward-fusion":
+        fbe = args.ff_bucket_elems if bucket_elems is None else bucket_elems
+
         def step():
-            of.run_forward_fusion(g, pol, (x, y), timing=False)
+            of.run_forward_fusion(g, pol, (x, y), timing=False, bucket_elems=fbe)
     else:
         def step():
             of.run_backward_fusion(g, pol, (x, y), workers=w, timing=False, bucket_elems=be)
@@ -290,6 +292,7 @@ def measure_in_situ(args, device, peaks, reps: int = 5) -> dict:
 
     from paper_2104_00237_b200.optim import bytes_per_element
     step, g, pol = make_runner(args, args.batch, "backward-fusion", device, workers=2)
+    # (launch groups as configured by --bucket-elems)
     for _ in range(3):
         step()
     eng = next(e for k, e in g._engines.items() if k[1])
@@ -361,22 +364,23 @@ def run_ours(args) -> dict:
     del step, g, pol
     if not args.no_extras:
         sched = {}
+        K = 1 << 18
         variants = [("torch.optim.SGD(foreach)", "baseline", None, None, "foreach", None),
                     ("torch.optim.SGD(fused)", "baseline", None, None, "fused", None),
                     ("ours:baseline", "baseline", None, None, None, None),
-                    ("ours:forward-fusion", "forward-fusion", None, None, None, None),
-                    ("ours:backward-fusion(w=1)", "backward-fusion", 1, None, None, 0),
-                    ("ours:backward-fusion(w=2)", "backward-fusion", 2, None, None, 0),
-                    ("ours:backward-fusion(w=2,zero)", "backward-fusion", 2, "zero", None, 0),
-                    ("ours:backward-fusion(w=1,bucket=256K)", "backward-fusion", 1, None, None, 1 << 18),
-                    ("ours:backward-fusion(w=2,bucket=256K)", "backward-fusion", 2, None, None, 1 << 18)]
+                    ("ours:forward-fusion(per-layer)", "forward-fusion", None, None, None, 0),
+                    ("ours:forward-fusion(bucket=256K)", "forward-fusion", None, None, None, K),
+                    ("ours:backward-fusion(w=1,per-layer)", "backward-fusion", 1, None, None, 0),
+                    ("ours:backward-fusion(w=2,per-layer)", "backward-fusion", 2, None, None, 0),
+                    ("ours:backward-fusion(w=1,bucket=256K)", "backward-fusion", 1, None, None, K),
+                    ("ours:backward-fusion(w=2,bucket=256K)", "backward-fusion", 2, None, None, K),
+                    ("ours:backward-fusion(w=2,bucket=256K,zero)", "backward-fusion", 2, "zero", None, K)]
+        sweep_rows = ("torch.optim.SGD(foreach)", "ours:forward-fusion(bucket=256K)",
+                      "ours:backward-fusion(w=2,bucket=256K)", "ours:backward-fusion(w=2,per-layer)")
         for b in [args.batch] + [int(s) for s in args.sweep.split(",") if s.strip()]:
             row = {}
             for name, sch, w, gr, opt, be in variants:
-                if b != args.batch and name not in ("torch.optim.SGD(foreach)",
-                                                    "ours:forward-fusion",
-                                                    "ours:backward-fusion(w=2)",
-                                                    "ours:backward-fusion(w=1,bucket=256K)"):
+                if b != args.batch and name not in sweep_rows:
                     continue
                 st, *_ = make_runner(args, b, sch, device, workers=w, grad_reset=gr, opt_impl=opt,
                                      bucket_elems=be)
@@ -423,7 +427,8 @@ def e2e(args, device, dist) -> dict:
     run = {"baseline": of.run_baseline, "forward-fusion": of.run_forward_fusion,
            "backward-fusion": of.run_backward_fusion}[args.schedule]
     kw = ({"workers": args.workers, "bucket_elems": args.bucket_elems}
-          if args.schedule == "backward-fusion" else {})
+          if args.schedule == "backward-fusion" else
+          {"bucket_elems": args.ff_bucket_elems} if args.schedule == "forward-fusion" else {})
 
     def step():
         x = xh.to(device, non_blocking=True)

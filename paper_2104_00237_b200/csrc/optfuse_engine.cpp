@@ -90,7 +90,7 @@ class Engine : public std::enable_shared_from_this<Engine> {
  public:
   Engine(std::vector<at::Tensor> params, std::vector<std::vector<int>> bf_groups,
          std::vector<std::vector<int>> layers, int64_t side_stream)
-      : params_(std::move(params)), layers_(std::move(layers)),
+      : params_(std::move(params)), layers_(std::move(layers)), ff_units_(layers_),
         side_(reinterpret_cast<cudaStream_t>(side_stream)) {
     const int np = static_cast<int>(params_.size());
     s0_.assign(np, at::Tensor());
@@ -240,10 +240,16 @@ class Engine : public std::enable_shared_from_this<Engine> {
     return c;
   }
 
-  // Updates the pending, not yet updated parameters of layer `li` on the
-  // current stream; returns how many were updated.
+  // Forward-fusion units: by default one per layer; set_ff_units replaces
+  // them by buckets of consecutive layers (execution order) whose updates
+  // are issued together before the bucket's first layer.
+  void set_ff_units(std::vector<std::vector<int>> units) { ff_units_ = std::move(units); }
+  void reset_ff_units() { ff_units_ = layers_; }
+
+  // Updates the pending, not yet updated parameters of forward-fusion unit
+  // `li` on the current stream; returns how many were updated.
   int ff_layer(int li) {
-    const auto& lp = layers_.at(li);
+    const auto& lp = ff_units_.at(li);
     scratch_.members.clear();
     for (int idx : lp)
       if (pending_[idx] && !updated_[idx]) scratch_.members.push_back(idx);
@@ -385,6 +391,7 @@ class Engine : public std::enable_shared_from_this<Engine> {
 
   std::vector<at::Tensor> params_, s0_, s1_;
   std::vector<std::vector<int>> layers_;
+  std::vector<std::vector<int>> ff_units_;
   std::vector<Group> groups_;
   Group scratch_;
   std::vector<int> group_of_, ready_;
@@ -434,6 +441,8 @@ PYBIND11_MODULE(_optfuse_engine, m) {
       .def("set_updated", &Engine::set_updated)
       .def("num_pending", &Engine::num_pending)
       .def("ff_layer", &Engine::ff_layer)
+      .def("set_ff_units", &Engine::set_ff_units)
+      .def("reset_ff_units", &Engine::reset_ff_units)
       .def("flush", &Engine::flush)
       .def("set_profile", &Engine::set_profile)
       .def("take_profile", &Engine::take_profile)

@@ -84,6 +84,8 @@ class FusionEngine:
             b = p.history[slots[1]] if len(slots) > 1 else None
             self.native.set_slots(p.id, a, b)
         self._hp_key = None
+        self.ff_bucket_elems = 0
+        self.ff_leaders = None
 
     def configure(self, policy, step_t: int, grad_scale=None) -> None:
         """Hyper-parameters (and the frozen step index) of the next launches."""

@@ -153,6 +153,8 @@ class Graph:
         self._flag_owner = None       # engine holding the pending/updated flags
         self._hook_owner = None       # engine whose C++ hooks sit on the parameters
         self._pre_handles = None
+        self._leader_handles = None   # bucketed forward fusion: hooks on bucket leaders only
+        self.exec_order = None        # layer indices in first-execution order (recorded)
 
     # -- structure ---------------------------------------------------------
 
@@ -205,6 +207,17 @@ class Graph:
             for h in self._pre_handles:
                 h.remove()
             self._pre_handles = None
+
+    def set_leader_hooks(self, leaders) -> None:
+        """Install forward pre-hooks on the given (layer, callback) pairs only,
+        replacing any previous leader hooks (``leaders=None`` removes them)."""
+        if self._leader_handles is not None:
+            for h in self._leader_handles:
+                h.remove()
+            self._leader_handles = None
+        if leaders:
+            self._leader_handles = [
+                L.module.register_forward_pre_hook(lambda m, a, fn=fn: fn()) for L, fn in leaders]
 
     def set_flag_owner(self, eng) -> None:
         """Move the forward-fusion flags into ``eng`` (a native engine) or back

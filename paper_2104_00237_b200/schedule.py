@@ -192,10 +192,20 @@ def _traced_backward(graph: Graph, policy: OptimizerPolicy, tc) -> None:
         eng.native.set_callback(None)
 
 
+def _leave_forward_fusion(graph: Graph, policy: OptimizerPolicy) -> None:
+    """Switching away from forward fusion: drop its leader hooks and apply any
+    update it still defers, so no schedule ever reads a stale parameter."""
+    graph.set_leader_hooks(None)
+    owner = graph._flag_owner
+    if owner is not None and owner.num_pending():
+        flush_pending_updates(graph, policy)
+
+
 def run_baseline(graph: Graph, policy: OptimizerPolicy, inp, *, timing: bool = True,
                  trace: bool = False) -> StepReport:
     """Three contiguous phases; the update phase is one multi-tensor launch."""
     _reject_newton(policy)
+    _leave_forward_fusion(graph, policy)
     policy.begin_iteration()
     tc = tr.ScheduleTrace(BASELINE) if trace else None
     marks = _Marks(timing)
@@ -221,8 +231,35 @@ def run_baseline(graph: Graph, policy: OptimizerPolicy, inp, *, timing: bool = T
     return StepReport(BASELINE, loss, tc, marks.events)
 
 
+def ff_units(graph: Graph, bucket_elems: int) -> tuple:
+    """Forward-fusion buckets over the recorded execution order: each
+    parameter goes to the bucket of the first layer that uses it; a bucket
+    closes once it holds ``bucket_elems`` elements.  Returns (units as lists
+    of parameter ids, leader layer of each unit)."""
+    units, leaders, seen = [], [], set()
+    cur, size, lead = [], 0, None
+    for li in graph.exec_order:
+        layer = graph.layers[li]
+        ids = [p.id for p in layer.params if p.id not in seen]
+        if not ids:
+            continue
+        seen.update(ids)
+        if lead is None:
+            lead = layer
+        cur += ids
+        size += sum(graph.parameters[i].value.numel() for i in ids)
+        if size >= bucket_elems:
+            units.append(cur)
+            leaders.append(lead)
+            cur, size, lead = [], 0, None
+    if cur:
+        units.append(cur)
+        leaders.append(lead)
+    return units, leaders
+
+
 def run_forward_fusion(graph: Graph, policy: OptimizerPolicy, inp, *, timing: bool = True,
-                       trace: bool = False) -> StepReport:
+                       trace: bool = False, bucket_elems: int = 0) -> StepReport:
     """Lazy schedule: deferred updates applied just before each layer's forward.
 
     The layer's forward pre-hook calls the native engine, which launches the
@@ -232,8 +269,15 @@ def run_forward_fusion(graph: Graph, policy: OptimizerPolicy, inp, *, timing: bo
     index (schedule.py:130-133).  Global-information transforms are legal: the
     clip factor is computed once all gradients exist and rides along with the
     deferred updates as a device scalar.
+
+    ``bucket_elems > 0`` groups consecutive layers (in the execution order
+    recorded by the first iteration) into buckets whose pending updates are
+    issued together right before the bucket's first layer, so only bucket
+    leaders carry a pre-hook.
     """
     _reject_newton(policy)
+    if bucket_elems < 0:
+        raise ConfigError(f"bucket_elems must be >= 0, got {bucket_elems}")
     eng = _engine(graph, policy, False)
     graph.set_flag_owner(eng.native)
     policy.begin_iteration()
@@ -242,16 +286,35 @@ def run_forward_fusion(graph: Graph, policy: OptimizerPolicy, inp, *, timing: bo
         eng.configure(policy, graph.pending_step_t, graph.pending_scale)
     native = eng.native
     ff_layer = native.ff_layer
-
-    if tc is None:
-        def apply_pending(layer):
-            ff_layer(layer.index)
-            return None
+    bucketed = bucket_elems > 0 and tc is None and graph.exec_order is not None
+    if bucketed:
+        if eng.ff_bucket_elems != bucket_elems:
+            units, leaders = ff_units(graph, bucket_elems)
+            native.set_ff_units(units)
+            eng.ff_bucket_elems = bucket_elems
+            eng.ff_leaders = [(L, (lambda i=i: ff_layer(i))) for i, L in enumerate(leaders)]
+        graph.set_leader_hooks(eng.ff_leaders)
+        apply_pending = None
     else:
-        def apply_pending(layer):
-            todo = [p.id for p in layer.params if p.pending and not p.updated]
-            ff_layer(layer.index)
-            return [tc.add_task(tr.OPT_STEP, pid, ()) for pid in todo]
+        if eng.ff_bucket_elems:
+            native.reset_ff_units()
+            eng.ff_bucket_elems = 0
+        graph.set_leader_hooks(None)
+        order = [] if graph.exec_order is None else None
+        seen = set()
+
+        if tc is None:
+            def apply_pending(layer):
+                if order is not None and layer.index not in seen:
+                    seen.add(layer.index)
+                    order.append(layer.index)
+                ff_layer(layer.index)
+                return None
+        else:
+            def apply_pending(layer):
+                todo = [p.id for p in layer.params if p.pending and not p.updated]
+                ff_layer(layer.index)
+                return [tc.add_task(tr.OPT_STEP, pid, ()) for pid in todo]
 
     marks = _Marks(timing)
     marks.mark()
@@ -260,6 +323,8 @@ def run_forward_fusion(graph: Graph, policy: OptimizerPolicy, inp, *, timing: bo
         loss = graph.forward(inp, tc)
     finally:
         graph._ff_hook = None
+    if not bucketed and tc is None and order is not None:
+        graph.exec_order = order
     # a pending parameter whose layer did not run this forward is applied now,
     # before this iteration's gradients accumulate on top of its old ones
     if native.num_pending():
@@ -334,6 +399,7 @@ def run_backward_fusion(graph: Graph, policy: OptimizerPolicy, inp, workers: int
         raise ConfigError(f"workers must be >= 1, got {workers}")
     if bucket_elems < 0:
         raise ConfigError(f"bucket_elems must be >= 0, got {bucket_elems}")
+    _leave_forward_fusion(graph, policy)
     eng = _engine(graph, policy, workers > 1, bucket_elems)
     policy.begin_iteration()
     eng.configure(policy, policy.t, None)
