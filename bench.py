@@ -213,6 +213,8 @@ def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
         net = g.module  # plain module: the Graph installs no hooks until a schedule runs
         kw = {"foreach": True} if opt_impl == "foreach" else {"fused": True}
         opt = torch.optim.SGD(net.parameters(), lr=0.1, momentum=0.9, weight_decay=5e-4, **kw)
+        if getattr(args, "world", 1) > 1:  # unfused data parallel: DDP all-reduce + torch.optim
+            net = torch.nn.parallel.DistributedDataParallel(net, device_ids=[device.index])
 
         def step():
             opt.zero_grad(set_to_none=True)
@@ -220,6 +222,18 @@ def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
             opt.step()
         return step, net, opt
 
+    if getattr(args, "world", 1) > 1:  # data parallel: sharded fused update over NCCL
+        from paper_2104_00237_b200.dp import DataParallelFusion
+        g = of.build_classifier(args.model, device=device, seed=seed)
+        g.track_counts = False
+        pol = of.OptimizerPolicy("sgd-momentum", eta=0.1, alpha=0.9, weight_decay=5e-4)
+        dpf = DataParallelFusion(g, pol)
+        run = {"baseline": dpf.run_baseline, "forward-fusion": dpf.run_forward_fusion,
+               "backward-fusion": dpf.run_backward_fusion}[schedule]
+
+        def step():
+            run((x, y))
+        return step, g, pol
     g = of.build_classifier(args.model, device=device, seed=seed)
     g.track_counts = False  # no per-layer Python pre-hooks unless a schedule needs them
     pol = of.OptimizerPolicy("sgd-momentum", eta=0.1, alpha=0.9, weight_decay=5e-4,
@@ -338,8 +352,7 @@ def run_ours(args) -> dict:
     torch.cuda.set_device(device)
     torch.backends.cudnn.benchmark = True
     peaks = load_peaks()
-    if dist.world > 1:
-        raise SystemExit("multi-GPU data parallel bench: see paper_2104_00237_b200.dp (not wired yet)")
+    args.world = dist.world
     flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=device)
     flush = flush_buf.zero_
 

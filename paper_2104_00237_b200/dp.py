@@ -1,0 +1,297 @@
+"""Data-parallel fused optimizer: per-bucket gradient reduce-scatter, sharded
+update, parameter all-gather.
+
+The reference is single-process; the paper only claims DDP compatibility
+(PAPER.md:1815-1818).  On B200 the update is element-wise and per-parameter,
+so it shards naturally: rank r owns a contiguous 1/W slice of every bucket
+(and only that slice of the optimizer history -- state memory / W).
+
+Layout (per bucket = consecutive layers in backward order, ``launch_groups``):
+  flat_param [padded]  -- the module's parameters become views into it
+  flat_grad  [padded]  -- ``param.grad`` views; AccumulateGrad adds in place
+  grad_shard [S], history shards [S] per slot, S = padded / W (padded to W*4
+  elements so every shard starts 16-byte aligned for the vector path)
+
+Backward fusion: when the last gradient of a bucket is accumulated, the
+bucket's pipeline is issued on the communication stream behind an event:
+``reduce_scatter_tensor(SUM)`` -> zero flat_grad -> the multi-tensor update
+kernel on the shard (1/W folded in as the device gradient scale) ->
+``all_gather_into_tensor`` back into flat_param.  It overlaps the backward of
+the remaining layers; the compute stream joins once at the end of backward.
+Forward fusion: the reduce-scatter happens in backward, the update +
+all-gather of each bucket are issued by its first layer's forward pre-hook,
+with the next bucket prefetched on the communication stream.
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from . import kernels
+from .engine import launch_groups
+from .errors import ConfigError, GlobalInfoRequired, StateError
+
+DEFAULT_BUCKET_ELEMS = 1 << 22  # 16 MiB of fp32 per bucket
+
+
+class _Bucket:
+    __slots__ = ("index", "params", "flat_param", "flat_grad", "grad_shard", "slots", "shard",
+                 "tl", "ready", "event", "done", "leader", "pending")
+
+    def __init__(self, index):
+        self.index = index
+
+
+class DataParallelFusion:
+    """Sharded fused optimizer of one Graph across a process group."""
+
+    def __init__(self, graph, policy, *, group=None, bucket_elems: int = DEFAULT_BUCKET_ELEMS,
+                 update_fn=None):
+        if not dist.is_initialized():
+            raise StateError("torch.distributed is not initialised")
+        if policy.kind == "newton":
+            raise ConfigError("newton has no per-parameter step")
+        self.graph = graph
+        self.policy = policy
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.update_fn = update_fn
+        self.device = graph.device
+        self.cuda = self.device.type == "cuda"
+        if self.cuda and update_fn is None:
+            kernels.sqnorm_workspace_len()  # the kernel library must load (no fallback)
+        elif update_fn is None:
+            raise ConfigError("the sharded update runs on CUDA; pass update_fn only for host tests")
+        self.comm = torch.cuda.Stream() if self.cuda else None
+        slots = policy.history_slots()
+        unit = self.world * 4
+        self.buckets = []
+        for bi, ids in enumerate(launch_groups(graph, bucket_elems)):
+            b = _Bucket(bi)
+            b.params = [graph.parameters[i] for i in ids]
+            dt = b.params[0].value.dtype
+            if any(p.value.dtype != dt for p in b.params):
+                raise ConfigError("a data-parallel bucket needs one dtype")
+            n = sum(p.value.numel() for p in b.params)
+            padded = -(-n // unit) * unit
+            S = padded // self.world
+            b.flat_param = torch.zeros(padded, dtype=dt, device=self.device)
+            b.flat_grad = torch.zeros(padded, dtype=dt, device=self.device)
+            off = 0
+            with torch.no_grad():
+                for p in b.params:
+                    v = p.value
+                    if not v.is_contiguous():
+                        raise ConfigError(f"parameter {p.id} must be contiguous for data parallel")
+                    k = v.numel()
+                    b.flat_param[off:off + k].copy_(v.reshape(-1))
+                    v.data = b.flat_param[off:off + k].view_as(v)
+                    v.grad = b.flat_grad[off:off + k].view_as(v)
+                    off += k
+            dist.broadcast(b.flat_param, src=dist.get_global_rank(group, 0) if group else 0,
+                           group=group)
+            b.shard = slice(self.rank * S, (self.rank + 1) * S)
+            b.grad_shard = torch.zeros(S, dtype=dt, device=self.device)
+            b.slots = {name: torch.zeros(S, dtype=dt, device=self.device) for name in slots}
+            if self.cuda:
+                tl = kernels.TensorList(1)
+                pv = b.flat_param[b.shard]
+                tl.set(0, pv, b.grad_shard, b.slots[slots[0]] if slots else None,
+                       b.slots[slots[1]] if len(slots) > 1 else None)
+                tl.set_dtypes(dt, dt)
+                b.tl = tl
+                b.event = torch.cuda.Event()
+                b.done = torch.cuda.Event()
+            b.ready = 0
+            b.pending = False
+            self.buckets.append(b)
+        self.bucket_of = {p.id: b for b in self.buckets for p in b.params}
+        self.scale = None
+        if self.cuda:
+            self.scale = torch.full((), 1.0 / self.world, dtype=torch.float32, device=self.device)
+        self._hooks = None
+        self._mode = None
+        self._leader_handles = None
+        self.join_event = torch.cuda.Event() if self.cuda else None
+
+    # -- the per-bucket pipeline ----------------------------------------------
+
+    def _reduce_scatter(self, b) -> None:
+        dist.reduce_scatter_tensor(b.grad_shard, b.flat_grad, op=dist.ReduceOp.SUM, group=self.group)
+        b.flat_grad.zero_()
+
+    def _update_and_gather(self, b, t: int) -> None:
+        if self.update_fn is not None:
+            b.grad_shard.mul_(1.0 / self.world)
+            self.update_fn(b.flat_param[b.shard], b.grad_shard, b.slots, t)
+        else:
+            kernels.policy_step(b.tl, self.policy._hparams(t), self.scale, 0, None)
+        dist.all_gather_into_tensor(b.flat_param, b.flat_param[b.shard], group=self.group)
+
+    def _on_stream(self, stream):
+        return torch.cuda.stream(stream) if stream is not None else _NullCtx()
+
+    # -- hooks -------------------------------------------------------------------
+
+    def _install(self) -> None:
+        if self._hooks is not None:
+            return
+        hooks = []
+        for p in self.graph.parameters:
+            hooks.append(p.value.register_post_accumulate_grad_hook(
+                lambda t, p=p: self._on_grad_ready(p)))
+        self._hooks = hooks
+
+    def _on_grad_ready(self, p) -> None:
+        b = self.bucket_of.get(p.id)
+        if b is None or self._mode is None:
+            return
+        b.ready += 1
+        if b.ready == len(b.params):
+            self._bucket_ready(b)
+
+    def _bucket_ready(self, b) -> None:
+        cur = torch.cuda.current_stream() if self.cuda else None
+        if self.cuda:
+            b.event.record(cur)
+            self.comm.wait_event(b.event)
+        with self._on_stream(self.comm):
+            self._reduce_scatter(b)
+            if self._mode == "backward-fusion":
+                self._update_and_gather(b, self.policy.t)
+            else:
+                b.pending = True
+            if self.cuda:
+                b.done.record(self.comm)
+
+    def _finish_backward(self) -> None:
+        for b in self.buckets:
+            if b.ready < len(b.params):  # parameters without gradients this iteration
+                self._bucket_ready(b)
+        if self.cuda:
+            self.join_event.record(self.comm)
+            torch.cuda.current_stream().wait_event(self.join_event)
+        for b in self.buckets:
+            b.ready = 0
+
+    # -- schedules -----------------------------------------------------------------
+
+    def run_backward_fusion(self, inp, *, timing: bool = False):
+        """Forward, then backward with each bucket's RS -> update -> AG issued
+        as soon as the bucket's gradients are complete."""
+        from .schedule import StepReport
+        pol = self.policy
+        if pol.requires_global_info:
+            raise GlobalInfoRequired("backward-fusion cannot host a global-information policy")
+        self._install()
+        self._apply_deferred()
+        pol.begin_iteration()
+        loss = self.graph.forward(inp)
+        self._mode = "backward-fusion"
+        try:
+            self.graph.backward()
+        finally:
+            pass
+        self._finish_backward()
+        self._mode = None
+        return StepReport("backward-fusion", loss, None, fused=True)
+
+    def run_baseline(self, inp, *, timing: bool = False):
+        """Unfused data parallel: full forward, full backward, then per bucket
+        RS -> update -> AG on the compute stream."""
+        from .schedule import StepReport
+        self._apply_deferred()
+        self.policy.begin_iteration()
+        loss = self.graph.forward(inp)
+        self.graph.backward()
+        for b in reversed(self.buckets):
+            self._reduce_scatter(b)
+            self._update_and_gather(b, self.policy.t)
+        return StepReport("baseline", loss, None)
+
+    def run_forward_fusion(self, inp, *, timing: bool = False):
+        """RS during backward; update + AG deferred to each bucket's first layer
+        in the next forward (next bucket prefetched on the comm stream)."""
+        from .schedule import StepReport
+        self._install()
+        self._install_leaders()
+        self.policy.begin_iteration()
+        loss = self.graph.forward(inp)
+        self._apply_deferred()          # buckets whose leader did not run
+        self._mode = "forward-fusion"
+        try:
+            self.graph.backward()
+        finally:
+            pass
+        self._finish_backward()
+        self._mode = None
+        self._pending_t = self.policy.t
+        return StepReport("forward-fusion", loss, None, fused=True,
+                          pending_updates=sum(len(b.params) for b in self.buckets if b.pending))
+
+    def _install_leaders(self) -> None:
+        if self._leader_handles is not None:
+            return
+        order = self.graph.exec_order or [L.index for L in self.graph.layers]
+        pos = {li: k for k, li in enumerate(order)}
+        fwd = []
+        for b in self.buckets:
+            first = min((pos.get(L.index, len(pos)) for p in b.params for L in p.layers))
+            fwd.append((first, b))
+        fwd.sort(key=lambda x: x[0])
+        self._fwd_buckets = [b for _, b in fwd]
+        handles = []
+        for k, (first, b) in enumerate(fwd):
+            if first >= len(order):
+                continue
+            layer = self.graph.layers[order[first]]
+            handles.append(layer.module.register_forward_pre_hook(
+                lambda m, a, k=k: self._leader(k)))
+        self._leader_handles = handles
+
+    def _leader(self, k: int):
+        bs = self._fwd_buckets
+        b = bs[k]
+        t = getattr(self, "_pending_t", None)
+        if b.pending:
+            if self.cuda:
+                torch.cuda.current_stream().wait_event(b.done)
+            self._issue_deferred(b, t, None)
+        if self.cuda:
+            torch.cuda.current_stream().wait_event(b.done)
+        if k + 1 < len(bs) and bs[k + 1].pending:   # prefetch the next bucket
+            nb = bs[k + 1]
+            self.comm.wait_stream(torch.cuda.current_stream()) if self.cuda else None
+            self._issue_deferred(nb, t, self.comm)
+        return None
+
+    def _issue_deferred(self, b, t, stream) -> None:
+        with self._on_stream(stream):
+            self._update_and_gather(b, t)
+            b.pending = False
+            if self.cuda:
+                b.done.record(torch.cuda.current_stream())
+
+    def _apply_deferred(self) -> None:
+        t = getattr(self, "_pending_t", None)
+        for b in self.buckets:
+            if b.pending:
+                if self.cuda:
+                    torch.cuda.current_stream().wait_event(b.done)
+                self._update_and_gather(b, t)
+                b.pending = False
+
+    def flush(self) -> int:
+        n = sum(len(b.params) for b in self.buckets if b.pending)
+        self._apply_deferred()
+        return n
+
+
+class _NullCtx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False

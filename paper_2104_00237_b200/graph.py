@@ -216,8 +216,13 @@ class Graph:
                 h.remove()
             self._leader_handles = None
         if leaders:
-            self._leader_handles = [
-                L.module.register_forward_pre_hook(lambda m, a, fn=fn: fn()) for L, fn in leaders]
+            def make(fn):
+                def hook(module, args):
+                    fn()
+                    return None  # a non-None return would replace the layer's input
+                return hook
+            self._leader_handles = [L.module.register_forward_pre_hook(make(fn))
+                                    for L, fn in leaders]
 
     def set_flag_owner(self, eng) -> None:
         """Move the forward-fusion flags into ``eng`` (a native engine) or back

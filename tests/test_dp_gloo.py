@@ -1,0 +1,98 @@
+"""Data-parallel plumbing (reduce-scatter -> sharded update -> all-gather) on
+CPU with the gloo backend, world size 2.
+
+The sharded update here is the numpy oracle (host stand-in for the sm_100a
+kernel, which the GPU tests cover); what is under test is the host logic:
+bucketing, padding, shard ownership, the collectives, bucket readiness from
+the gradient hooks, forward-fusion deferral and the 1/W averaging.  The
+result must equal a single process that averages both ranks' gradients and
+applies the reference update -- bit for bit.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+KIND, ETA, WD = "adam", 1e-2, 1e-3
+ITERS = 4
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _inputs(rank):
+    rng = np.random.default_rng(100 + rank)
+    return [torch.from_numpy(rng.uniform(0.1, 1.0, (3, 6)).astype(np.float32)) for _ in range(ITERS)]
+
+
+def _oracle_update(theta, grad, slots, t):
+    from oracle import optim_ref
+    hp = optim_ref.Hyper(kind=KIND, eta=ETA, weight_decay=WD)
+    np_slots = {k: v.numpy() for k, v in slots.items()}
+    optim_ref.step(KIND, hp, theta.numpy(), grad.numpy(), np_slots, t)
+
+
+def _worker(rank, world, port, schedule, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2104_00237_b200 as of
+        from paper_2104_00237_b200.dp import DataParallelFusion
+        g = of.build_model("shared-chain", layers=4, width=6, device="cpu", exact=False,
+                           track_input_grad=False)
+        pol = of.OptimizerPolicy(KIND, eta=ETA, weight_decay=WD)
+        dp = DataParallelFusion(g, pol, bucket_elems=40, update_fn=_oracle_update)
+        assert len(dp.buckets) >= 2
+        run = {"backward-fusion": dp.run_backward_fusion, "baseline": dp.run_baseline,
+               "forward-fusion": dp.run_forward_fusion}[schedule]
+        for x in _inputs(rank):
+            run(x)
+        dp.flush()
+        flat = np.concatenate([p.value.detach().numpy().reshape(-1) for p in g.parameters])
+        out[rank] = flat.tobytes()
+    finally:
+        dist.destroy_process_group()
+
+
+def _single_process_reference():
+    import paper_2104_00237_b200 as of
+    from oracle import optim_ref
+    g = of.build_model("shared-chain", layers=4, width=6, device="cpu", exact=False,
+                       track_input_grad=False)
+    hp = optim_ref.Hyper(kind=KIND, eta=ETA, weight_decay=WD)
+    slots = [dict() for _ in g.parameters]
+    xs = [_inputs(r) for r in range(2)]
+    for it in range(ITERS):
+        grads = []
+        for r in range(2):
+            for p in g.parameters:
+                p.value.grad = None
+            g.module(xs[r][it]).backward()
+            grads.append([p.value.grad.numpy().reshape(-1).copy() for p in g.parameters])
+        for k, p in enumerate(g.parameters):
+            avg = (grads[0][k] + grads[1][k]) * np.float32(0.5)
+            theta = p.value.detach().numpy().reshape(-1)
+            optim_ref.step(KIND, hp, theta, avg, slots[k], it + 1)
+    return np.concatenate([p.value.detach().numpy().reshape(-1) for p in g.parameters]).tobytes()
+
+
+@pytest.mark.parametrize("schedule", ["backward-fusion", "baseline", "forward-fusion"])
+def test_sharded_update_equals_single_process(schedule):
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().dict()
+    mp.start_processes(_worker, args=(2, _free_port(), schedule, out), nprocs=2, join=True,
+                       start_method="spawn")
+    assert out[0] == out[1], "ranks disagree after the all-gather"
+    want = _single_process_reference()
+    got = np.frombuffer(out[0], np.float32)
+    ref = np.frombuffer(want, np.float32)
+    assert got.tobytes() == ref.tobytes(), np.abs(got - ref).max()

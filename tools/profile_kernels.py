@@ -1,0 +1,40 @@
+"""Workloads for ncu captures of the update kernel (run under ncu, never timed).
+
+    python tools/profile_kernels.py bf      # MobileNetV2 b128 backward fusion, bucketed launches
+    python tools/profile_kernels.py vgg     # one multi-tensor Adam launch over VGG-16 (138 M params)
+"""
+
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+import torch  # noqa: E402
+
+import paper_2104_00237_b200 as of  # noqa: E402
+from paper_2104_00237_b200.models import synthetic_batch  # noqa: E402
+
+
+def bf(iters=6):
+    g = of.build_classifier("mobilenet_v2_cifar", device="cuda")
+    g.track_counts = False
+    pol = of.OptimizerPolicy("sgd-momentum", eta=0.1, alpha=0.9, weight_decay=5e-4, grad_reset="none")
+    x, y = synthetic_batch("mobilenet_v2_cifar", 128, device="cuda")
+    for _ in range(iters):
+        of.run_backward_fusion(g, pol, (x, y), workers=2, bucket_elems=1 << 18, timing=False)
+    torch.cuda.synchronize()
+
+
+def vgg(iters=3):
+    g = of.build_classifier("vgg16", device="cuda")
+    pol = of.OptimizerPolicy("adam", eta=1e-4)
+    for p in g.parameters:
+        p.value.grad = torch.randn_like(p.value) * 0.01
+    for _ in range(iters):
+        pol.begin_iteration()
+        pol.step_params(g.parameters)
+    torch.cuda.synchronize()
+
+
+if __name__ == "__main__":
+    {"bf": bf, "vgg": vgg}[sys.argv[1]]()
