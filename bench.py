@@ -372,7 +372,10 @@ def run_ours(args) -> dict:
                       "workers": args.workers, "grad_reset": args.grad_reset,
                       "bucket_elems": args.bucket_elems,
                       "parallelism": f"dp{dist.world}",
-                      "l2": "256 MiB buffer zeroed before every timed step (inside the timed region)"},
+                      "l2": "256 MiB buffer zeroed before every timed step (inside the timed region)",
+                      "model_math": ("fp32 parameters/activations; cuDNN convolutions with PyTorch's "
+                                     f"default TF32 policy (allow_tf32={torch.backends.cudnn.allow_tf32}); "
+                                     "optimizer update exact fp32 (reference arithmetic)")},
            "gpu_launches": launches}
     del step, g, pol
     if not args.no_extras:
