@@ -63,6 +63,8 @@ def parse_args(argv=None):
                     help="backward-fusion launch groups: 0 = one per layer, else merge layers "
                          "(backward order) into buckets of at least this many elements")
     ap.add_argument("--sweep", default="32,64,256,512", help="extra per-GPU batches ('' to skip)")
+    ap.add_argument("--graphs", type=int, default=0,
+                    help="1: capture each iteration (ours and the torch baseline) as a CUDA graph")
     ap.add_argument("--no-extras", action="store_true", help="headline only (for profilers)")
     ap.add_argument("--cpu-iters", type=int, default=2, help="CPU baseline sample iterations")
     return ap.parse_args(argv)
@@ -199,14 +201,17 @@ def load_peaks() -> dict:
 # ---------------------------------------------------------------------------
 
 def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
-                grad_reset=None, opt_impl=None, bucket_elems=None):
-    """Returns (step_fn, graph_or_model, policy_or_opt)."""
+                grad_reset=None, opt_impl=None, bucket_elems=None, graphed=None):
+    """Returns (step_fn, graph_or_model, policy_or_opt); ``graphed`` captures
+    the whole iteration as a CUDA graph (paper_2104_00237_b200.graphs)."""
     import torch
     import torch.nn.functional as F
 
     import paper_2104_00237_b200 as of
+    from paper_2104_00237_b200.graphs import CapturedStep
     from paper_2104_00237_b200.models import synthetic_batch
 
+    graphed = args.graphs if graphed is None else graphed
     x, y = synthetic_batch(args.model, batch, device=device, seed=seed)
     if opt_impl is not None:  # unfused torch.optim baseline
         g = of.build_classifier(args.model, device=device, seed=seed)
@@ -215,43 +220,53 @@ def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
         opt = torch.optim.SGD(net.parameters(), lr=0.1, momentum=0.9, weight_decay=5e-4, **kw)
         if getattr(args, "world", 1) > 1:  # unfused data parallel: DDP all-reduce + torch.optim
             net = torch.nn.parallel.DistributedDataParallel(net, device_ids=[device.index])
+            graphed = False
 
-        def step():
+        def run(inp):
             opt.zero_grad(set_to_none=True)
-            F.cross_entropy(net(x), y).backward()
+            loss = F.cross_entropy(net(inp[0]), inp[1])
+            loss.backward()
             opt.step()
-        return step, net, opt
-
-    if getattr(args, "world", 1) > 1:  # data parallel: sharded fused update over NCCL
+            return loss
+        owner, pol = net, opt
+    elif getattr(args, "world", 1) > 1:  # data parallel: sharded fused update over NCCL
         from paper_2104_00237_b200.dp import DataParallelFusion
         g = of.build_classifier(args.model, device=device, seed=seed)
         g.track_counts = False
         pol = of.OptimizerPolicy("sgd-momentum", eta=0.1, alpha=0.9, weight_decay=5e-4)
         dpf = DataParallelFusion(g, pol)
-        run = {"baseline": dpf.run_baseline, "forward-fusion": dpf.run_forward_fusion,
-               "backward-fusion": dpf.run_backward_fusion}[schedule]
+        dp_run = {"baseline": dpf.run_baseline, "forward-fusion": dpf.run_forward_fusion,
+                  "backward-fusion": dpf.run_backward_fusion}[schedule]
+        graphed = False
 
-        def step():
-            run((x, y))
-        return step, g, pol
-    g = of.build_classifier(args.model, device=device, seed=seed)
-    g.track_counts = False  # no per-layer Python pre-hooks unless a schedule needs them
-    pol = of.OptimizerPolicy("sgd-momentum", eta=0.1, alpha=0.9, weight_decay=5e-4,
-                             grad_reset=grad_reset or args.grad_reset)
-    w = args.workers if workers is None else workers
-    be = args.bucket_elems if bucket_elems is None else bucket_elems
-    if schedule == "baseline":
-        def step():
-            of.run_baseline(g, pol, (x, y), timing=False)
-    elif schedule == "forward-fusion":
-        fbe = args.ff_bucket_elems if bucket_elems is None else bucket_elems
-
-        def step():
-            of.run_forward_fusion(g, pol, (x, y), timing=False, bucket_elems=fbe)
+        def run(inp):
+            return dp_run(inp).loss
+        owner = g
     else:
-        def step():
-            of.run_backward_fusion(g, pol, (x, y), workers=w, timing=False, bucket_elems=be)
-    return step, g, pol
+        g = of.build_classifier(args.model, device=device, seed=seed)
+        g.track_counts = False  # no per-layer Python pre-hooks unless a schedule needs them
+        pol = of.OptimizerPolicy("sgd-momentum", eta=0.1, alpha=0.9, weight_decay=5e-4,
+                                 grad_reset=grad_reset or args.grad_reset)
+        w = args.workers if workers is None else workers
+        if schedule == "baseline":
+            def run(inp):
+                return of.run_baseline(g, pol, inp, timing=False).loss
+        elif schedule == "forward-fusion":
+            fbe = args.ff_bucket_elems if bucket_elems is None else bucket_elems
+
+            def run(inp):
+                return of.run_forward_fusion(g, pol, inp, timing=False, bucket_elems=fbe).loss
+        else:
+            be = args.bucket_elems if bucket_elems is None else bucket_elems
+
+            def run(inp):
+                return of.run_backward_fusion(g, pol, inp, workers=w, timing=False,
+                                              bucket_elems=be).loss
+        owner = g
+    if graphed:
+        cap = CapturedStep(run, (x, y), warmup=3)
+        return cap, owner, pol
+    return (lambda: run((x, y))), owner, pol
 
 
 def measure_update_kernel(args, device, peaks) -> dict:
@@ -370,7 +385,7 @@ def run_ours(args) -> dict:
            "config": {"workload": WORKLOAD, "model": args.model, "batch_per_gpu": args.batch,
                       "global_batch": args.batch * dist.world, "schedule": args.schedule,
                       "workers": args.workers, "grad_reset": args.grad_reset,
-                      "bucket_elems": args.bucket_elems,
+                      "bucket_elems": args.bucket_elems, "cuda_graph": bool(args.graphs),
                       "parallelism": f"dp{dist.world}",
                       "l2": "256 MiB buffer zeroed before every timed step (inside the timed region)",
                       "model_math": ("fp32 parameters/activations; cuDNN convolutions with PyTorch's "
@@ -381,32 +396,45 @@ def run_ours(args) -> dict:
     if not args.no_extras:
         sched = {}
         K = 1 << 18
-        variants = [("torch.optim.SGD(foreach)", "baseline", None, None, "foreach", None),
-                    ("torch.optim.SGD(fused)", "baseline", None, None, "fused", None),
-                    ("ours:baseline", "baseline", None, None, None, None),
-                    ("ours:forward-fusion(per-layer)", "forward-fusion", None, None, None, 0),
-                    ("ours:forward-fusion(bucket=256K)", "forward-fusion", None, None, None, K),
-                    ("ours:backward-fusion(w=1,per-layer)", "backward-fusion", 1, None, None, 0),
-                    ("ours:backward-fusion(w=2,per-layer)", "backward-fusion", 2, None, None, 0),
-                    ("ours:backward-fusion(w=1,bucket=256K)", "backward-fusion", 1, None, None, K),
-                    ("ours:backward-fusion(w=2,bucket=256K)", "backward-fusion", 2, None, None, K),
-                    ("ours:backward-fusion(w=2,bucket=256K,zero)", "backward-fusion", 2, "zero", None, K)]
+        # (name, schedule, workers, grad_reset, torch optimizer, bucket elems, CUDA graph)
+        variants = [("torch.optim.SGD(foreach)", "baseline", None, None, "foreach", None, False),
+                    ("torch.optim.SGD(fused)", "baseline", None, None, "fused", None, False),
+                    ("ours:baseline", "baseline", None, None, None, None, False),
+                    ("ours:forward-fusion(per-layer)", "forward-fusion", None, None, None, 0, False),
+                    ("ours:forward-fusion(bucket=256K)", "forward-fusion", None, None, None, K, False),
+                    ("ours:backward-fusion(w=1,per-layer)", "backward-fusion", 1, None, None, 0, False),
+                    ("ours:backward-fusion(w=2,per-layer)", "backward-fusion", 2, None, None, 0, False),
+                    ("ours:backward-fusion(w=1,bucket=256K)", "backward-fusion", 1, None, None, K, False),
+                    ("ours:backward-fusion(w=2,bucket=256K)", "backward-fusion", 2, None, None, K, False),
+                    ("ours:backward-fusion(w=2,bucket=256K,zero)", "backward-fusion", 2, "zero", None, K, False),
+                    ("graph:torch.optim.SGD(foreach)", "baseline", None, None, "foreach", None, True),
+                    ("graph:ours:baseline", "baseline", None, None, None, None, True),
+                    ("graph:ours:forward-fusion(bucket=256K)", "forward-fusion", None, None, None, K, True),
+                    ("graph:ours:backward-fusion(w=2,per-layer)", "backward-fusion", 2, None, None, 0, True),
+                    ("graph:ours:backward-fusion(w=2,bucket=256K)", "backward-fusion", 2, None, None, K, True)]
+        if dist.world > 1:
+            variants = [v for v in variants if not v[6]]
         sweep_rows = ("torch.optim.SGD(foreach)", "ours:forward-fusion(bucket=256K)",
-                      "ours:backward-fusion(w=2,bucket=256K)", "ours:backward-fusion(w=2,per-layer)")
+                      "ours:backward-fusion(w=2,bucket=256K)", "ours:backward-fusion(w=2,per-layer)",
+                      "graph:torch.optim.SGD(foreach)", "graph:ours:backward-fusion(w=2,bucket=256K)",
+                      "graph:ours:forward-fusion(bucket=256K)")
         for b in [args.batch] + [int(s) for s in args.sweep.split(",") if s.strip()]:
             row = {}
-            for name, sch, w, gr, opt, be in variants:
+            for name, sch, w, gr, opt, be, gph in variants:
                 if b != args.batch and name not in sweep_rows:
                     continue
                 st, *_ = make_runner(args, b, sch, device, workers=w, grad_reset=gr, opt_impl=opt,
-                                     bucket_elems=be)
+                                     bucket_elems=be, graphed=gph)
                 t = timed(st, args.steps, args.warmup, dist, flush)
                 row[name] = {"ms_per_step": round(t, 4), "images_per_s": round(b * 1e3 / t, 1)}
                 del st
                 torch.cuda.empty_cache()
             base = row["torch.optim.SGD(foreach)"]["ms_per_step"]
+            gbase = row.get("graph:torch.optim.SGD(foreach)", {}).get("ms_per_step")
             for k, v in row.items():
                 v["speedup_vs_torch_foreach"] = round(base / v["ms_per_step"], 4)
+                if gbase and k.startswith("graph:"):
+                    v["speedup_vs_graphed_torch_foreach"] = round(gbase / v["ms_per_step"], 4)
             sched[str(b)] = row
         res["schedules"] = sched
         base_ms = sched[str(args.batch)]["torch.optim.SGD(foreach)"]["ms_per_step"]
@@ -446,11 +474,19 @@ def e2e(args, device, dist) -> dict:
           if args.schedule == "backward-fusion" else
           {"bucket_elems": args.ff_bucket_elems} if args.schedule == "forward-fusion" else {})
 
-    def step():
-        x = xh.to(device, non_blocking=True)
-        y = yh.to(device, non_blocking=True)
-        rep = run(g, pol, (x, y), timing=False, **kw)
-        return rep.loss.item()
+    if args.graphs:
+        from paper_2104_00237_b200.graphs import CapturedStep
+        static = (xh.to(device), yh.to(device))
+        cap = CapturedStep(lambda inp: run(g, pol, inp, timing=False, **kw).loss, static, policy=pol)
+
+        def step():
+            return cap((xh, yh)).item()     # pinned host -> static device buffers, replay, loss -> host
+    else:
+        def step():
+            x = xh.to(device, non_blocking=True)
+            y = yh.to(device, non_blocking=True)
+            rep = run(g, pol, (x, y), timing=False, **kw)
+            return rep.loss.item()
 
     for _ in range(args.warmup):
         step()
