@@ -65,6 +65,7 @@ def parse_args(argv=None):
     ap.add_argument("--sweep", default="32,64,256,512", help="extra per-GPU batches ('' to skip)")
     ap.add_argument("--graphs", type=int, default=0,
                     help="1: capture each iteration (ours and the torch baseline) as a CUDA graph")
+    ap.add_argument("--channels-last", type=int, default=0, help="1: NHWC model and inputs")
     ap.add_argument("--no-extras", action="store_true", help="headline only (for profilers)")
     ap.add_argument("--cpu-iters", type=int, default=2, help="CPU baseline sample iterations")
     return ap.parse_args(argv)
@@ -200,10 +201,23 @@ def load_peaks() -> dict:
 # our arm
 # ---------------------------------------------------------------------------
 
+# BASELINE.json configs measured here: C2 (the headline) and C3 (update-bound)
+WORKLOADS = {
+    "c2": {"model": "mobilenet_v2_cifar", "batch": 128, "kind": "sgd-momentum",
+           "hp": {"eta": 0.1, "alpha": 0.9, "weight_decay": 5e-4},
+           "torch": ("SGD", {"lr": 0.1, "momentum": 0.9, "weight_decay": 5e-4})},
+    "c3": {"model": "vgg16", "batch": 32, "kind": "adam",
+           "hp": {"eta": 1e-4, "weight_decay": 1e-4},
+           "torch": ("Adam", {"lr": 1e-4, "weight_decay": 1e-4})},
+}
+
+
 def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
-                grad_reset=None, opt_impl=None, bucket_elems=None, graphed=None):
-    """Returns (step_fn, graph_or_model, policy_or_opt); ``graphed`` captures
-    the whole iteration as a CUDA graph (paper_2104_00237_b200.graphs)."""
+                grad_reset=None, opt_impl=None, bucket_elems=None, graphed=None,
+                workload="c2", channels_last=None):
+    """Returns (step_fn, graph_or_model, policy_or_opt).  ``opt_impl`` selects
+    the unfused torch.optim baseline ("foreach" | "fused"); ``graphed``
+    captures the whole iteration as a CUDA graph (paper_2104_00237_b200.graphs)."""
     import torch
     import torch.nn.functional as F
 
@@ -211,14 +225,22 @@ def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
     from paper_2104_00237_b200.graphs import CapturedStep
     from paper_2104_00237_b200.models import synthetic_batch
 
+    wl = WORKLOADS[workload]
     graphed = args.graphs if graphed is None else graphed
-    x, y = synthetic_batch(args.model, batch, device=device, seed=seed)
+    cl = args.channels_last if channels_last is None else channels_last
+    x, y = synthetic_batch(wl["model"], batch, device=device, seed=seed)
+    if cl:
+        x = x.contiguous(memory_format=torch.channels_last)
+    world = getattr(args, "world", 1)
     if opt_impl is not None:  # unfused torch.optim baseline
-        g = of.build_classifier(args.model, device=device, seed=seed)
+        g = of.build_classifier(wl["model"], device=device, seed=seed, channels_last=bool(cl))
         net = g.module  # plain module: the Graph installs no hooks until a schedule runs
-        kw = {"foreach": True} if opt_impl == "foreach" else {"fused": True}
-        opt = torch.optim.SGD(net.parameters(), lr=0.1, momentum=0.9, weight_decay=5e-4, **kw)
-        if getattr(args, "world", 1) > 1:  # unfused data parallel: DDP all-reduce + torch.optim
+        name, kw = wl["torch"]
+        kw = dict(kw, **({"foreach": True} if opt_impl == "foreach" else {"fused": True}))
+        if graphed and name == "Adam":
+            kw["capturable"] = True
+        opt = getattr(torch.optim, name)(net.parameters(), **kw)
+        if world > 1:  # unfused data parallel: DDP all-reduce + torch.optim
             net = torch.nn.parallel.DistributedDataParallel(net, device_ids=[device.index])
             graphed = False
 
@@ -229,11 +251,11 @@ def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
             opt.step()
             return loss
         owner, pol = net, opt
-    elif getattr(args, "world", 1) > 1:  # data parallel: sharded fused update over NCCL
+    elif world > 1:  # data parallel: sharded fused update over NCCL
         from paper_2104_00237_b200.dp import DataParallelFusion
-        g = of.build_classifier(args.model, device=device, seed=seed)
+        g = of.build_classifier(wl["model"], device=device, seed=seed)
         g.track_counts = False
-        pol = of.OptimizerPolicy("sgd-momentum", eta=0.1, alpha=0.9, weight_decay=5e-4)
+        pol = of.OptimizerPolicy(wl["kind"], **wl["hp"])
         dpf = DataParallelFusion(g, pol)
         dp_run = {"baseline": dpf.run_baseline, "forward-fusion": dpf.run_forward_fusion,
                   "backward-fusion": dpf.run_backward_fusion}[schedule]
@@ -243,10 +265,9 @@ def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
             return dp_run(inp).loss
         owner = g
     else:
-        g = of.build_classifier(args.model, device=device, seed=seed)
+        g = of.build_classifier(wl["model"], device=device, seed=seed, channels_last=bool(cl))
         g.track_counts = False  # no per-layer Python pre-hooks unless a schedule needs them
-        pol = of.OptimizerPolicy("sgd-momentum", eta=0.1, alpha=0.9, weight_decay=5e-4,
-                                 grad_reset=grad_reset or args.grad_reset)
+        pol = of.OptimizerPolicy(wl["kind"], **wl["hp"], grad_reset=grad_reset or args.grad_reset)
         w = args.workers if workers is None else workers
         if schedule == "baseline":
             def run(inp):
@@ -264,9 +285,14 @@ def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
                                               bucket_elems=be).loss
         owner = g
     if graphed:
-        cap = CapturedStep(run, (x, y), warmup=3)
+        cap = CapturedStep(run, (x, y), warmup=3,
+                           policy=pol if isinstance(pol, of.OptimizerPolicy) else None)
         return cap, owner, pol
-    return (lambda: run((x, y))), owner, pol
+
+    def step():
+        return run((x, y))
+    step.run = run
+    return step, owner, pol
 
 
 def measure_update_kernel(args, device, peaks) -> dict:
@@ -320,7 +346,7 @@ def measure_in_situ(args, device, peaks, reps: int = 5) -> dict:
     import torch
 
     from paper_2104_00237_b200.optim import bytes_per_element
-    step, g, pol = make_runner(args, args.batch, "backward-fusion", device, workers=2)
+    step, g, pol = make_runner(args, args.batch, "backward-fusion", device, workers=2, graphed=False)
     # (launch groups as configured by --bucket-elems)
     for _ in range(3):
         step()
@@ -358,6 +384,53 @@ def cpu_baseline(args, iters: int) -> dict:
                        f"over {r['update_elems']} params)")}
 
 
+def _variants_c2(world: int):
+    """(name, schedule, workers, grad_reset, torch optimizer, bucket, CUDA graph, channels-last)"""
+    K = 1 << 18
+    v = [("torch.optim.SGD(foreach)", "baseline", None, None, "foreach", None, False, False),
+         ("torch.optim.SGD(fused)", "baseline", None, None, "fused", None, False, False),
+         ("ours:baseline", "baseline", None, None, None, None, False, False),
+         ("ours:forward-fusion(per-layer)", "forward-fusion", None, None, None, 0, False, False),
+         ("ours:forward-fusion(bucket=256K)", "forward-fusion", None, None, None, K, False, False),
+         ("ours:backward-fusion(w=1,per-layer)", "backward-fusion", 1, None, None, 0, False, False),
+         ("ours:backward-fusion(w=2,per-layer)", "backward-fusion", 2, None, None, 0, False, False),
+         ("ours:backward-fusion(w=1,bucket=256K)", "backward-fusion", 1, None, None, K, False, False),
+         ("ours:backward-fusion(w=2,bucket=256K)", "backward-fusion", 2, None, None, K, False, False),
+         ("ours:backward-fusion(w=2,bucket=256K,zero)", "backward-fusion", 2, "zero", None, K, False, False),
+         ("graph:torch.optim.SGD(foreach)", "baseline", None, None, "foreach", None, True, False),
+         ("graph:torch.optim.SGD(fused)", "baseline", None, None, "fused", None, True, False),
+         ("graph:ours:baseline", "baseline", None, None, None, None, True, False),
+         ("graph:ours:forward-fusion(bucket=256K)", "forward-fusion", None, None, None, K, True, False),
+         ("graph:ours:backward-fusion(w=2,per-layer)", "backward-fusion", 2, None, None, 0, True, False),
+         ("graph:ours:backward-fusion(w=2,bucket=256K)", "backward-fusion", 2, None, None, K, True, False),
+         ("cl:torch.optim.SGD(foreach)", "baseline", None, None, "foreach", None, False, True),
+         ("cl:ours:backward-fusion(w=2,bucket=256K)", "backward-fusion", 2, None, None, K, False, True),
+         ("cl:graph:torch.optim.SGD(foreach)", "baseline", None, None, "foreach", None, True, True),
+         ("cl:graph:ours:backward-fusion(w=2,bucket=256K)", "backward-fusion", 2, None, None, K, True, True),
+         ("cl:graph:ours:forward-fusion(bucket=256K)", "forward-fusion", None, None, None, K, True, True)]
+    if world > 1:
+        v = [x for x in v if not x[6]]
+    return v
+
+
+SWEEP_ROWS = ("torch.optim.SGD(foreach)", "ours:forward-fusion(bucket=256K)",
+              "ours:backward-fusion(w=2,bucket=256K)", "graph:torch.optim.SGD(foreach)",
+              "graph:ours:backward-fusion(w=2,bucket=256K)", "graph:ours:forward-fusion(bucket=256K)")
+
+
+def _speedups(row: dict) -> None:
+    """Speed-ups against the matching unfused torch baseline (same graph /
+    layout mode)."""
+    for k, v in row.items():
+        mode = k.rsplit("ours:", 1)[0] if "ours:" in k else k.rsplit("torch.optim", 1)[0]
+        base = row.get(mode + "torch.optim.SGD(foreach)") or row.get(mode + "torch.optim.Adam(foreach)")
+        if base:
+            v["speedup_vs_unfused_same_mode"] = round(base["ms_per_step"] / v["ms_per_step"], 4)
+        eager = row.get("torch.optim.SGD(foreach)") or row.get("torch.optim.Adam(foreach)")
+        if eager:
+            v["speedup_vs_eager_torch_foreach"] = round(eager["ms_per_step"] / v["ms_per_step"], 4)
+
+
 def run_ours(args) -> dict:
     import torch
 
@@ -375,7 +448,10 @@ def run_ours(args) -> dict:
     n0 = _native.launch_count()
     with Clocks(dist.local) as clk:
         ms = timed(step, args.steps, args.warmup, dist, flush)
-    launches = (_native.launch_count() - n0) * args.steps // (args.steps + args.warmup)
+    if hasattr(step, "native_launches"):   # CUDA graph: kernel nodes replayed per step
+        launches = step.native_launches * args.steps
+    else:
+        launches = (_native.launch_count() - n0) * args.steps // (args.steps + args.warmup)
     clocks = clk.summary()
     value = dist.world * args.batch * 1e3 / ms
     res = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": dist.world,
@@ -386,60 +462,34 @@ def run_ours(args) -> dict:
                       "global_batch": args.batch * dist.world, "schedule": args.schedule,
                       "workers": args.workers, "grad_reset": args.grad_reset,
                       "bucket_elems": args.bucket_elems, "cuda_graph": bool(args.graphs),
+                      "channels_last": bool(args.channels_last),
                       "parallelism": f"dp{dist.world}",
                       "l2": "256 MiB buffer zeroed before every timed step (inside the timed region)",
                       "model_math": ("fp32 parameters/activations; cuDNN convolutions with PyTorch's "
                                      f"default TF32 policy (allow_tf32={torch.backends.cudnn.allow_tf32}); "
                                      "optimizer update exact fp32 (reference arithmetic)")},
-           "gpu_launches": launches}
+           "gpu_launches": int(launches)}
     del step, g, pol
+    torch.cuda.empty_cache()
     if not args.no_extras:
         sched = {}
-        K = 1 << 18
-        # (name, schedule, workers, grad_reset, torch optimizer, bucket elems, CUDA graph)
-        variants = [("torch.optim.SGD(foreach)", "baseline", None, None, "foreach", None, False),
-                    ("torch.optim.SGD(fused)", "baseline", None, None, "fused", None, False),
-                    ("ours:baseline", "baseline", None, None, None, None, False),
-                    ("ours:forward-fusion(per-layer)", "forward-fusion", None, None, None, 0, False),
-                    ("ours:forward-fusion(bucket=256K)", "forward-fusion", None, None, None, K, False),
-                    ("ours:backward-fusion(w=1,per-layer)", "backward-fusion", 1, None, None, 0, False),
-                    ("ours:backward-fusion(w=2,per-layer)", "backward-fusion", 2, None, None, 0, False),
-                    ("ours:backward-fusion(w=1,bucket=256K)", "backward-fusion", 1, None, None, K, False),
-                    ("ours:backward-fusion(w=2,bucket=256K)", "backward-fusion", 2, None, None, K, False),
-                    ("ours:backward-fusion(w=2,bucket=256K,zero)", "backward-fusion", 2, "zero", None, K, False),
-                    ("graph:torch.optim.SGD(foreach)", "baseline", None, None, "foreach", None, True),
-                    ("graph:ours:baseline", "baseline", None, None, None, None, True),
-                    ("graph:ours:forward-fusion(bucket=256K)", "forward-fusion", None, None, None, K, True),
-                    ("graph:ours:backward-fusion(w=2,per-layer)", "backward-fusion", 2, None, None, 0, True),
-                    ("graph:ours:backward-fusion(w=2,bucket=256K)", "backward-fusion", 2, None, None, K, True)]
-        if dist.world > 1:
-            variants = [v for v in variants if not v[6]]
-        sweep_rows = ("torch.optim.SGD(foreach)", "ours:forward-fusion(bucket=256K)",
-                      "ours:backward-fusion(w=2,bucket=256K)", "ours:backward-fusion(w=2,per-layer)",
-                      "graph:torch.optim.SGD(foreach)", "graph:ours:backward-fusion(w=2,bucket=256K)",
-                      "graph:ours:forward-fusion(bucket=256K)")
-        for b in [args.batch] + [int(s) for s in args.sweep.split(",") if s.strip()]:
+        for b in [args.batch] + [int(x) for x in args.sweep.split(",") if x.strip()]:
             row = {}
-            for name, sch, w, gr, opt, be, gph in variants:
-                if b != args.batch and name not in sweep_rows:
+            for name, sch, w, gr, opt, be, gph, cl in _variants_c2(dist.world):
+                if b != args.batch and name not in SWEEP_ROWS:
                     continue
                 st, *_ = make_runner(args, b, sch, device, workers=w, grad_reset=gr, opt_impl=opt,
-                                     bucket_elems=be, graphed=gph)
+                                     bucket_elems=be, graphed=gph, channels_last=cl)
                 t = timed(st, args.steps, args.warmup, dist, flush)
-                row[name] = {"ms_per_step": round(t, 4), "images_per_s": round(b * 1e3 / t, 1)}
+                row[name] = {"ms_per_step": round(t, 4), "images_per_s": round(dist.world * b * 1e3 / t, 1)}
                 del st
                 torch.cuda.empty_cache()
-            base = row["torch.optim.SGD(foreach)"]["ms_per_step"]
-            gbase = row.get("graph:torch.optim.SGD(foreach)", {}).get("ms_per_step")
-            for k, v in row.items():
-                v["speedup_vs_torch_foreach"] = round(base / v["ms_per_step"], 4)
-                if gbase and k.startswith("graph:"):
-                    v["speedup_vs_graphed_torch_foreach"] = round(gbase / v["ms_per_step"], 4)
+            _speedups(row)
             sched[str(b)] = row
         res["schedules"] = sched
         base_ms = sched[str(args.batch)]["torch.optim.SGD(foreach)"]["ms_per_step"]
         res["speedup_vs_unfused_torch"] = round(base_ms / ms, 4)
-        # end to end through the public API: pinned host batch -> device, loss -> host
+        res["c3_vgg16_adam"] = run_c3(args, device, dist, flush)
         res["e2e"] = e2e(args, device, dist)
         ins = measure_in_situ(args, device, peaks, 5)
         std = measure_update_kernel(args, device, peaks)
@@ -457,44 +507,53 @@ def run_ours(args) -> dict:
     return res
 
 
+def run_c3(args, device, dist, flush) -> dict:
+    """C3 (BASELINE.json configs[2]): VGG-16, 3x224x224, batch 32 per GPU, Adam with
+    coupled weight decay 1e-4 (the paper's setting) -- the update-bound case."""
+    import torch
+    b = WORKLOADS["c3"]["batch"]
+    steps, warm = max(args.steps // 3, 5), 3
+    row = {}
+    for name, sch, w, opt in (("torch.optim.Adam(foreach)", "baseline", None, "foreach"),
+                              ("torch.optim.Adam(fused)", "baseline", None, "fused"),
+                              ("ours:baseline", "baseline", None, None),
+                              ("ours:forward-fusion(per-layer)", "forward-fusion", None, None),
+                              ("ours:backward-fusion(w=2,per-layer)", "backward-fusion", 2, None)):
+        st, *_ = make_runner(args, b, sch, device, workers=w, opt_impl=opt, bucket_elems=0,
+                             graphed=False, workload="c3", channels_last=False)
+        t = timed(st, steps, warm, dist, flush)
+        row[name] = {"ms_per_step": round(t, 3), "images_per_s": round(dist.world * b * 1e3 / t, 1)}
+        del st
+        torch.cuda.empty_cache()
+    _speedups(row)
+    return {"batch_per_gpu": b, "steps": steps, "warmup": warm, "eager": True, "schedules": row}
+
+
 def e2e(args, device, dist) -> dict:
+    """The headline configuration through the public API, end to end: each
+    step copies the batch from pinned host memory to the device and reads the
+    loss back (CapturedStep copies into its static buffers, then replays)."""
     import torch
 
-    import paper_2104_00237_b200 as of
     from paper_2104_00237_b200.models import synthetic_batch
-    xh, yh = synthetic_batch(args.model, args.batch, device="cpu")
+    xh, yh = synthetic_batch(args.model, args.batch, device="cpu", seed=1)
     xh, yh = xh.pin_memory(), yh.pin_memory()
-    g = of.build_classifier(args.model, device=device)
-    g.track_counts = False
-    pol = of.OptimizerPolicy("sgd-momentum", eta=0.1, alpha=0.9, weight_decay=5e-4,
-                             grad_reset=args.grad_reset)
-    run = {"baseline": of.run_baseline, "forward-fusion": of.run_forward_fusion,
-           "backward-fusion": of.run_backward_fusion}[args.schedule]
-    kw = ({"workers": args.workers, "bucket_elems": args.bucket_elems}
-          if args.schedule == "backward-fusion" else
-          {"bucket_elems": args.ff_bucket_elems} if args.schedule == "forward-fusion" else {})
-
-    if args.graphs:
-        from paper_2104_00237_b200.graphs import CapturedStep
-        static = (xh.to(device), yh.to(device))
-        cap = CapturedStep(lambda inp: run(g, pol, inp, timing=False, **kw).loss, static, policy=pol)
-
-        def step():
-            return cap((xh, yh)).item()     # pinned host -> static device buffers, replay, loss -> host
+    step, g, pol = make_runner(args, args.batch, args.schedule, device)
+    if hasattr(step, "graph"):
+        def one():
+            return step((xh, yh)).item()
     else:
-        def step():
-            x = xh.to(device, non_blocking=True)
-            y = yh.to(device, non_blocking=True)
-            rep = run(g, pol, (x, y), timing=False, **kw)
-            return rep.loss.item()
+        run = step.run
 
+        def one():
+            return run((xh.to(device, non_blocking=True), yh.to(device, non_blocking=True))).item()
     for _ in range(args.warmup):
-        step()
+        one()
     torch.cuda.synchronize()
     dist.barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        step()
+        one()
     torch.cuda.synchronize()
     dt = dist.max(time.perf_counter() - t0)
     return {"value": round(dist.world * args.batch * args.steps / dt, 2), "unit": UNIT,

@@ -45,9 +45,13 @@ class CapturedStep:
                 step_fn(self._arg())
         cur.wait_stream(side)
         torch.cuda.synchronize()
+        from . import _native
+        n0 = _native.launch_count()
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
             self.loss = step_fn(self._arg())
+        # liboptfuse_b200 kernel nodes in the graph (each replay launches them all)
+        self.native_launches = _native.launch_count() - n0
 
     def _arg(self):
         return self.static if len(self.static) > 1 else self.static[0]
