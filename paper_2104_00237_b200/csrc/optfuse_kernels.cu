@@ -267,13 +267,17 @@ __device__ __forceinline__ bool aligned(const void* p, unsigned a) {
   return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0;
 }
 
-// One multi-tensor policy step.  T: param/state type; G: grad type.
-template <class Op, class T, class G, int CAP>
+// One multi-tensor policy step.  T: param/state type; G: grad type; UNR:
+// vectors per thread per tile (tile = 256 * 4 * UNR elements).  Small lists
+// use UNR=1 so that even a few MB spread over more CTAs than there are SMs.
+template <class Op, class T, class G, int CAP, int UNR>
 __global__ void __launch_bounds__(kThreads)
 mt_step_kernel(const __grid_constant__ MTParams<CAP> mp, const Op op,
                const float* __restrict__ gscale, uint32_t flags) {
   using GV = typename GradVal<G>::type;
-  constexpr int kRound = sizeof(T) == 8 ? 2 : 4;  // vectors in flight per thread per round
+  constexpr int kTileU = kThreads * kVec * UNR;
+  constexpr int kRoundMax = sizeof(T) == 8 ? 2 : 4;
+  constexpr int kRound = UNR < kRoundMax ? UNR : kRoundMax;  // vectors in flight per thread
   const int total = mp.tile_end[mp.count - 1];
   const bool zero_grad = (flags & OF_FLAG_ZERO_GRAD) != 0;
   const bool shadow = (flags & OF_FLAG_SHADOW_BF16) != 0;
@@ -283,9 +287,9 @@ mt_step_kernel(const __grid_constant__ MTParams<CAP> mp, const Op op,
   for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
     while (tile >= mp.tile_end[ti]) ++ti;
     const int tfirst = ti ? mp.tile_end[ti - 1] : 0;
-    const int64_t base = static_cast<int64_t>(tile - tfirst) * kTile;
+    const int64_t base = static_cast<int64_t>(tile - tfirst) * kTileU;
     const int64_t rem = mp.n[ti] - base;
-    const int len = rem < kTile ? static_cast<int>(rem) : kTile;
+    const int len = rem < kTileU ? static_cast<int>(rem) : kTileU;
     T* p = static_cast<T*>(mp.p[ti]) + base;
     G* g = static_cast<G*>(mp.g[ti]) + base;
     T* s0 = Op::kSlots >= 1 ? static_cast<T*>(mp.s0[ti]) + base : nullptr;
@@ -298,7 +302,7 @@ mt_step_kernel(const __grid_constant__ MTParams<CAP> mp, const Op op,
     if (vec_ok) {
       const int nvec = len / kVec;
 #pragma unroll
-      for (int r = 0; r < kUnroll; r += kRound) {
+      for (int r = 0; r < UNR; r += kRound) {
         T vp[kRound][4], v0[kRound][4], v1[kRound][4];
         GV vg[kRound][4];
 #pragma unroll
@@ -445,7 +449,7 @@ int validate_list(const of_tensor_list* l, int slots, bool need_shadow, bool gra
 
 // Packs tensors [first, first+count) into a parameter block; returns total tiles.
 template <int CAP>
-int64_t pack(const of_tensor_list* l, int first, int count, MTParams<CAP>& mp) {
+int64_t pack(const of_tensor_list* l, int first, int count, MTParams<CAP>& mp, int tile = kTile) {
   int64_t tiles = 0;
   mp.count = count;
   for (int i = 0; i < count; ++i) {
@@ -456,7 +460,7 @@ int64_t pack(const of_tensor_list* l, int first, int count, MTParams<CAP>& mp) {
     mp.s1[i] = l->state1 ? l->state1[k] : nullptr;
     mp.sh[i] = l->shadow ? l->shadow[k] : nullptr;
     mp.n[i] = l->numel[k];
-    tiles += (l->numel[k] + kTile - 1) / kTile;
+    tiles += (l->numel[k] + tile - 1) / tile;
     mp.tile_end[i] = static_cast<int32_t>(tiles);
   }
   return tiles;
@@ -466,12 +470,19 @@ template <class Op, class T, class G, int CAP>
 int launch_step_chunk(const of_tensor_list* l, int first, int count, const Op& op,
                       const float* gscale, uint32_t flags, cudaStream_t s) {
   MTParams<CAP> mp;
-  const int64_t tiles = pack<CAP>(l, first, count, mp);
+  int64_t tiles = pack<CAP>(l, first, count, mp, kTile);
   if (tiles == 0) return OF_OK;
-  if (tiles > INT32_MAX) return fail(OF_ERR_INVALID, "tensor list too large for one launch");
   const int64_t cap = static_cast<int64_t>(sm_count()) * kCtasPerSm;
+  if (tiles < 2 * static_cast<int64_t>(sm_count())) {
+    // small launch: 1024-element tiles, 4x the CTAs for the same bytes
+    tiles = pack<CAP>(l, first, count, mp, kThreads * kVec);
+    const int grid = static_cast<int>(tiles < cap ? tiles : cap);
+    mt_step_kernel<Op, T, G, CAP, 1><<<grid, kThreads, 0, s>>>(mp, op, gscale, flags);
+    return check_launch("mt_step_kernel");
+  }
+  if (tiles > INT32_MAX) return fail(OF_ERR_INVALID, "tensor list too large for one launch");
   const int grid = static_cast<int>(tiles < cap ? tiles : cap);
-  mt_step_kernel<Op, T, G, CAP><<<grid, kThreads, 0, s>>>(mp, op, gscale, flags);
+  mt_step_kernel<Op, T, G, CAP, kUnroll><<<grid, kThreads, 0, s>>>(mp, op, gscale, flags);
   return check_launch("mt_step_kernel");
 }
 
