@@ -63,9 +63,9 @@ def parse_args(argv=None):
                     help="backward-fusion launch groups: 0 = one per layer, else merge layers "
                          "(backward order) into buckets of at least this many elements")
     ap.add_argument("--sweep", default="32,64,256,512", help="extra per-GPU batches ('' to skip)")
-    ap.add_argument("--graphs", type=int, default=0,
+    ap.add_argument("--graphs", type=int, default=1,
                     help="1: capture each iteration (ours and the torch baseline) as a CUDA graph")
-    ap.add_argument("--channels-last", type=int, default=0, help="1: NHWC model and inputs")
+    ap.add_argument("--channels-last", type=int, default=1, help="1: NHWC model and inputs")
     ap.add_argument("--no-extras", action="store_true", help="headline only (for profilers)")
     ap.add_argument("--cpu-iters", type=int, default=2, help="CPU baseline sample iterations")
     return ap.parse_args(argv)
@@ -269,6 +269,9 @@ def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
         g.track_counts = False  # no per-layer Python pre-hooks unless a schedule needs them
         pol = of.OptimizerPolicy(wl["kind"], **wl["hp"], grad_reset=grad_reset or args.grad_reset)
         w = args.workers if workers is None else workers
+        ctas = None
+        if w == 0:        # side stream with an uncapped update grid
+            w, ctas = 2, 0
         if schedule == "baseline":
             def run(inp):
                 return of.run_baseline(g, pol, inp, timing=False).loss
@@ -282,7 +285,7 @@ def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
 
             def run(inp):
                 return of.run_backward_fusion(g, pol, inp, workers=w, timing=False,
-                                              bucket_elems=be).loss
+                                              bucket_elems=be, update_ctas=ctas).loss
         owner = g
     if graphed:
         cap = CapturedStep(run, (x, y), warmup=3,
@@ -359,7 +362,7 @@ def measure_in_situ(args, device, peaks, reps: int = 5) -> dict:
             torch.cuda._sleep(20_000_000)
         native.set_profile(True)
         for gi in range(native.num_groups):
-            native.launch_group(gi)
+            native.launch_group(gi, sync=False)   # queued behind the sleep: kernel time only
         native.set_profile(False)
         native.join()
         recs += native.take_profile()
@@ -518,7 +521,8 @@ def run_c3(args, device, dist, flush) -> dict:
                               ("torch.optim.Adam(fused)", "baseline", None, "fused"),
                               ("ours:baseline", "baseline", None, None),
                               ("ours:forward-fusion(per-layer)", "forward-fusion", None, None),
-                              ("ours:backward-fusion(w=2,per-layer)", "backward-fusion", 2, None)):
+                              ("ours:backward-fusion(w=2,per-layer)", "backward-fusion", 2, None),
+                              ("ours:backward-fusion(w=2,per-layer,uncapped)", "backward-fusion", 0, None)):
         st, *_ = make_runner(args, b, sch, device, workers=w, opt_impl=opt, bucket_elems=0,
                              graphed=False, workload="c3", channels_last=False)
         t = timed(st, steps, warm, dist, flush)

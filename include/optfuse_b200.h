@@ -78,7 +78,9 @@ typedef enum of_kind {
  * Python doubles; the library rounds them to the tensor precision. */
 typedef struct of_hparams {
   int32_t kind;            /* of_kind */
-  int32_t reserved;
+  int32_t max_ctas;        /* launch at most this many CTAs (0 = fill the GPU): a
+                              backward-fusion update on a side stream keeps most
+                              SMs free for the backward it overlaps */
   double eta;              /* step size */
   double alpha;            /* momentum decay */
   double weight_decay;     /* coupled for SGD..ADAM (optim.py:102-104), decoupled for ADAMW */

@@ -35,7 +35,7 @@ _PP = ctypes.POINTER(ctypes.c_void_p)
 
 
 class OfHparams(ctypes.Structure):
-    _fields_ = [("kind", ctypes.c_int32), ("reserved", ctypes.c_int32),
+    _fields_ = [("kind", ctypes.c_int32), ("max_ctas", ctypes.c_int32),
                 ("eta", ctypes.c_double), ("alpha", ctypes.c_double),
                 ("weight_decay", ctypes.c_double), ("epsilon", ctypes.c_double),
                 ("beta1", ctypes.c_double), ("beta2", ctypes.c_double), ("rho", ctypes.c_double),

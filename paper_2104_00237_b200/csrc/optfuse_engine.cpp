@@ -136,8 +136,9 @@ class Engine : public std::enable_shared_from_this<Engine> {
 
   void set_hparams(int kind, double eta, double alpha, double wd, double eps, double b1, double b2,
                    double rho, double bc1, double bc2, int64_t flags, bool release_grads,
-                   c10::optional<at::Tensor> grad_scale) {
+                   c10::optional<at::Tensor> grad_scale, int max_ctas) {
     hp_.kind = kind;
+    hp_.max_ctas = max_ctas;
     hp_.eta = eta;
     hp_.alpha = alpha;
     hp_.weight_decay = wd;
@@ -293,8 +294,10 @@ class Engine : public std::enable_shared_from_this<Engine> {
     return out;
   }
 
-  // Launches group `gi` now (as its last gradient-ready hook would).
-  void launch_now(int gi) { launch_group(gi); }
+  // Launches group `gi` now, as its last gradient-ready hook would (sync: with
+  // the event edge from the current stream; without it for back-to-back
+  // timing replays on a stream the caller has already ordered).
+  void launch_now(int gi, bool sync) { launch_group(gi, sync); }
 
   int64_t launches() const { return launches_; }
   int num_groups() const { return static_cast<int>(groups_.size()); }
@@ -355,12 +358,12 @@ class Engine : public std::enable_shared_from_this<Engine> {
     ++launches_;
   }
 
-  void launch_group(int gi) {
+  void launch_group(int gi, bool sync = true) {
     Group& G = groups_[gi];
     fill_grads(G);
     cudaStream_t cur = current();
-    cudaStream_t s = cur;
-    if (side_) {
+    cudaStream_t s = side_ ? side_ : cur;
+    if (side_ && sync) {
       cuda_check(cudaEventRecord(G.ready, cur), "cudaEventRecord");
       cuda_check(cudaStreamWaitEvent(side_, G.ready, 0), "cudaStreamWaitEvent");
       s = side_;
@@ -446,7 +449,7 @@ PYBIND11_MODULE(_optfuse_engine, m) {
       .def("flush", &Engine::flush)
       .def("set_profile", &Engine::set_profile)
       .def("take_profile", &Engine::take_profile)
-      .def("launch_group", &Engine::launch_now)
+      .def("launch_group", &Engine::launch_now, py::arg("gi"), py::arg("sync") = true)
       .def_property_readonly("launches", &Engine::launches)
       .def_property_readonly("num_groups", &Engine::num_groups);
 }

@@ -468,12 +468,13 @@ int64_t pack(const of_tensor_list* l, int first, int count, MTParams<CAP>& mp, i
 
 template <class Op, class T, class G, int CAP>
 int launch_step_chunk(const of_tensor_list* l, int first, int count, const Op& op,
-                      const float* gscale, uint32_t flags, cudaStream_t s) {
+                      const float* gscale, uint32_t flags, int max_ctas, cudaStream_t s) {
   MTParams<CAP> mp;
   int64_t tiles = pack<CAP>(l, first, count, mp, kTile);
   if (tiles == 0) return OF_OK;
-  const int64_t cap = static_cast<int64_t>(sm_count()) * kCtasPerSm;
-  if (tiles < 2 * static_cast<int64_t>(sm_count())) {
+  int64_t cap = static_cast<int64_t>(sm_count()) * kCtasPerSm;
+  if (max_ctas > 0 && max_ctas < cap) cap = max_ctas;
+  if (tiles < 2 * static_cast<int64_t>(sm_count()) && max_ctas == 0) {
     // small launch: 1024-element tiles, 4x the CTAs for the same bytes
     tiles = pack<CAP>(l, first, count, mp, kThreads * kVec);
     const int grid = static_cast<int>(tiles < cap ? tiles : cap);
@@ -488,20 +489,20 @@ int launch_step_chunk(const of_tensor_list* l, int first, int count, const Op& o
 
 template <class Op, class T, class G>
 int launch_step(const of_tensor_list* l, const Op& op, const float* gscale, uint32_t flags,
-                cudaStream_t s) {
+                int max_ctas, cudaStream_t s) {
   int first = 0;
   while (first < l->n) {
     const int left = l->n - first;
     int st;
     if (left <= 4) {
-      st = launch_step_chunk<Op, T, G, 4>(l, first, left, op, gscale, flags, s);
+      st = launch_step_chunk<Op, T, G, 4>(l, first, left, op, gscale, flags, max_ctas, s);
       first += left;
     } else if (left <= 16) {
-      st = launch_step_chunk<Op, T, G, 16>(l, first, left, op, gscale, flags, s);
+      st = launch_step_chunk<Op, T, G, 16>(l, first, left, op, gscale, flags, max_ctas, s);
       first += left;
     } else {
       const int c = left < 64 ? left : 64;
-      st = launch_step_chunk<Op, T, G, 64>(l, first, c, op, gscale, flags, s);
+      st = launch_step_chunk<Op, T, G, 64>(l, first, c, op, gscale, flags, max_ctas, s);
       first += c;
     }
     if (st != OF_OK) return st;
@@ -521,32 +522,32 @@ int dispatch_kind(const of_tensor_list* l, const of_hparams* hp, const float* gs
   switch (hp->kind) {
     case OF_SGD: {
       SgdOp<T> op{coupled<T>(hp), neg_eta};
-      return launch_step<SgdOp<T>, T, G>(l, op, gscale, flags, s);
+      return launch_step<SgdOp<T>, T, G>(l, op, gscale, flags, hp->max_ctas, s);
     }
     case OF_SGD_MOMENTUM: {
       SgdMomentumOp<T> op{coupled<T>(hp), neg_eta, static_cast<T>(hp->alpha)};
-      return launch_step<SgdMomentumOp<T>, T, G>(l, op, gscale, flags, s);
+      return launch_step<SgdMomentumOp<T>, T, G>(l, op, gscale, flags, hp->max_ctas, s);
     }
     case OF_ADAGRAD: {
       AdagradOp<T> op{coupled<T>(hp), neg_eta, static_cast<T>(hp->epsilon)};
-      return launch_step<AdagradOp<T>, T, G>(l, op, gscale, flags, s);
+      return launch_step<AdagradOp<T>, T, G>(l, op, gscale, flags, hp->max_ctas, s);
     }
     case OF_RMSPROP: {
       RmspropOp<T> op{coupled<T>(hp), neg_eta, static_cast<T>(hp->epsilon),
                       static_cast<T>(hp->rho), static_cast<T>(1.0 - hp->rho)};
-      return launch_step<RmspropOp<T>, T, G>(l, op, gscale, flags, s);
+      return launch_step<RmspropOp<T>, T, G>(l, op, gscale, flags, hp->max_ctas, s);
     }
     case OF_ADADELTA: {
       AdadeltaOp<T> op{coupled<T>(hp), neg_eta, static_cast<T>(hp->epsilon),
                        static_cast<T>(hp->rho), static_cast<T>(1.0 - hp->rho)};
-      return launch_step<AdadeltaOp<T>, T, G>(l, op, gscale, flags, s);
+      return launch_step<AdadeltaOp<T>, T, G>(l, op, gscale, flags, hp->max_ctas, s);
     }
     case OF_ADAM: {
       AdamOp<T> op{coupled<T>(hp), neg_eta, static_cast<T>(hp->epsilon),
                    static_cast<T>(hp->beta1), static_cast<T>(hp->beta2),
                    static_cast<T>(1.0 - hp->beta1), static_cast<T>(1.0 - hp->beta2),
                    static_cast<T>(hp->bias_correction1), static_cast<T>(hp->bias_correction2)};
-      return launch_step<AdamOp<T>, T, G>(l, op, gscale, flags, s);
+      return launch_step<AdamOp<T>, T, G>(l, op, gscale, flags, hp->max_ctas, s);
     }
     case OF_ADAMW: {
       const double w1 = 1.0 - hp->beta1;
@@ -555,7 +556,7 @@ int dispatch_kind(const of_tensor_list* l, const of_hparams* hp, const float* gs
                     static_cast<T>(std::sqrt(hp->bias_correction2)), static_cast<T>(hp->epsilon),
                     static_cast<T>(-(hp->eta / hp->bias_correction1)),
                     hp->weight_decay != 0.0, std::fabs(w1) < 0.5};
-      return launch_step<AdamWOp<T>, T, G>(l, op, gscale, flags, s);
+      return launch_step<AdamWOp<T>, T, G>(l, op, gscale, flags, hp->max_ctas, s);
     }
     default:
       return fail(OF_ERR_INVALID, "unknown optimizer kind %d", hp->kind);
@@ -636,6 +637,7 @@ int of_policy_step_mt(const of_tensor_list* list, const of_hparams* hp,
     return fail(OF_ERR_INVALID, "adam bias corrections must be non-zero (step index t >= 1)");
   int st = validate_list(list, slots, (flags & OF_FLAG_SHADOW_BF16) != 0, false);
   if (st != OF_OK || list->n == 0) return st;
+  if (hp->max_ctas < 0) return fail(OF_ERR_INVALID, "max_ctas must be >= 0, got %d", hp->max_ctas);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (list->param_dtype == OF_F64) return dispatch_kind<double, double>(list, hp, grad_scale_dev, flags, s);
   if (list->grad_dtype == OF_BF16) return dispatch_kind<float, __nv_bfloat16>(list, hp, grad_scale_dev, flags, s);

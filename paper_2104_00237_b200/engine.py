@@ -87,10 +87,11 @@ class FusionEngine:
         self.ff_bucket_elems = 0
         self.ff_leaders = None
 
-    def configure(self, policy, step_t: int, grad_scale=None) -> None:
-        """Hyper-parameters (and the frozen step index) of the next launches."""
+    def configure(self, policy, step_t: int, grad_scale=None, max_ctas: int = 0) -> None:
+        """Hyper-parameters (and the frozen step index) of the next launches.
+        ``max_ctas`` caps each update's grid (0: fill the GPU)."""
         key = (step_t, policy.kind, policy.eta, policy.alpha, policy.weight_decay, policy.epsilon,
-               policy.beta1, policy.beta2, policy.rho, policy.grad_reset, id(grad_scale))
+               policy.beta1, policy.beta2, policy.rho, policy.grad_reset, id(grad_scale), max_ctas)
         if key == self._hp_key:
             return
         hp = kernels.hparams(policy.kind, policy.eta, policy.alpha, policy.weight_decay,
@@ -98,7 +99,8 @@ class FusionEngine:
         zero = policy.grad_reset == "zero"
         self.native.set_hparams(hp.kind, hp.eta, hp.alpha, hp.weight_decay, hp.epsilon, hp.beta1,
                                 hp.beta2, hp.rho, hp.bias_correction1, hp.bias_correction2,
-                                nat.OF_FLAG_ZERO_GRAD if zero else 0, not zero, grad_scale)
+                                nat.OF_FLAG_ZERO_GRAD if zero else 0, not zero, grad_scale,
+                                max_ctas)
         self._hp_key = key
 
     @property

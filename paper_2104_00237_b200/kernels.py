@@ -62,14 +62,14 @@ class TensorList:
 
 
 def hparams(kind: str, eta: float, alpha: float, weight_decay: float, epsilon: float,
-            beta1: float, beta2: float, rho: float, t: int) -> nat.OfHparams:
+            beta1: float, beta2: float, rho: float, t: int, max_ctas: int = 0) -> nat.OfHparams:
     """of_hparams for step index t; bias corrections in double (optim.py:145-146)."""
     bc1 = bc2 = 1.0
     if kind in ("adam", "adamw"):
         bc1 = 1 - beta1 ** t
         bc2 = 1 - beta2 ** t
-    return nat.OfHparams(nat.KIND_CODES[kind], 0, eta, alpha, weight_decay, epsilon, beta1,
-                         beta2, rho, bc1, bc2)
+    return nat.OfHparams(nat.KIND_CODES[kind], max_ctas, eta, alpha, weight_decay, epsilon,
+                         beta1, beta2, rho, bc1, bc2)
 
 
 def policy_step(tl: TensorList, hp: nat.OfHparams, grad_scale, flags: int, stream) -> None:

@@ -377,16 +377,26 @@ def flush_pending_updates(graph: Graph, policy: OptimizerPolicy,
     return n
 
 
+def default_update_ctas() -> int:
+    """Grid cap of a side-stream backward-fusion update: a third of the SMs
+    (~2 TB/s of HBM streaming) so the update overlaps the backward kernels
+    instead of time-slicing with them."""
+    return max(8, torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count // 3)
+
+
 def run_backward_fusion(graph: Graph, policy: OptimizerPolicy, inp, workers: int = 1, *,
                         timing: bool = True, trace: bool = False,
-                        bucket_elems: int = 0) -> StepReport:
+                        bucket_elems: int = 0, update_ctas: int | None = None) -> StepReport:
     """Eager schedule: update each layer as soon as its gradients are complete.
 
     ``workers=1`` issues each update inline on the autograd stream;
     ``workers>1`` on the engine's high-priority side stream behind an event
     (the device half of the Appendix B.2 guard), overlapping the backward of
-    the preceding layers.  ``bucket_elems`` merges consecutive layers (backward
-    order) into launch groups of at least that many elements.
+    the preceding layers; there each update's grid is capped at
+    ``update_ctas`` CTAs (default: a third of the SMs; 0 = uncapped) so it
+    streams alongside the backward instead of displacing it.
+    ``bucket_elems`` merges consecutive layers (backward order) into launch
+    groups of at least that many elements.
     Raises GlobalInfoRequired, mutating nothing, for policies or transforms
     that must see all gradients first (schedule.py:174-177).
     """
@@ -402,7 +412,9 @@ def run_backward_fusion(graph: Graph, policy: OptimizerPolicy, inp, workers: int
     _leave_forward_fusion(graph, policy)
     eng = _engine(graph, policy, workers > 1, bucket_elems)
     policy.begin_iteration()
-    eng.configure(policy, policy.t, None)
+    if workers > 1 and update_ctas is None:
+        update_ctas = default_update_ctas()
+    eng.configure(policy, policy.t, None, update_ctas if workers > 1 else 0)
     tc = tr.ScheduleTrace(BACKWARD_FUSION) if trace else None
     marks = _Marks(timing)
     marks.mark()
