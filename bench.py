@@ -270,8 +270,8 @@ def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
         pol = of.OptimizerPolicy(wl["kind"], **wl["hp"], grad_reset=grad_reset or args.grad_reset)
         w = args.workers if workers is None else workers
         ctas = None
-        if w == 0:        # side stream with an uncapped update grid
-            w, ctas = 2, 0
+        if w == -1:       # side stream with the update grid capped to a third of the SMs
+            w, ctas = 2, max(8, torch.cuda.get_device_properties(device).multi_processor_count // 3)
         if schedule == "baseline":
             def run(inp):
                 return of.run_baseline(g, pol, inp, timing=False).loss
@@ -410,7 +410,11 @@ def _variants_c2(world: int):
          ("cl:ours:backward-fusion(w=2,bucket=256K)", "backward-fusion", 2, None, None, K, False, True),
          ("cl:graph:torch.optim.SGD(foreach)", "baseline", None, None, "foreach", None, True, True),
          ("cl:graph:ours:backward-fusion(w=2,bucket=256K)", "backward-fusion", 2, None, None, K, True, True),
-         ("cl:graph:ours:forward-fusion(bucket=256K)", "forward-fusion", None, None, None, K, True, True)]
+         ("cl:graph:ours:forward-fusion(bucket=256K)", "forward-fusion", None, None, None, K, True, True),
+         ("cl:graph:ours:backward-fusion(w=2,bucket=1M)", "backward-fusion", 2, None, None, 4 * K, True, True),
+         ("cl:graph:ours:backward-fusion(w=2,bucket=4M)", "backward-fusion", 2, None, None, 16 * K, True, True),
+         ("cl:graph:ours:backward-fusion(w=1,bucket=256K)", "backward-fusion", 1, None, None, K, True, True),
+         ("cl:graph:ours:forward-fusion(bucket=1M)", "forward-fusion", None, None, None, 4 * K, True, True)]
     if world > 1:
         v = [x for x in v if not x[6]]
     return v
@@ -522,7 +526,7 @@ def run_c3(args, device, dist, flush) -> dict:
                               ("ours:baseline", "baseline", None, None),
                               ("ours:forward-fusion(per-layer)", "forward-fusion", None, None),
                               ("ours:backward-fusion(w=2,per-layer)", "backward-fusion", 2, None),
-                              ("ours:backward-fusion(w=2,per-layer,uncapped)", "backward-fusion", 0, None)):
+                              ("ours:backward-fusion(w=2,per-layer,capped)", "backward-fusion", -1, None)):
         st, *_ = make_runner(args, b, sch, device, workers=w, opt_impl=opt, bucket_elems=0,
                              graphed=False, workload="c3", channels_last=False)
         t = timed(st, steps, warm, dist, flush)

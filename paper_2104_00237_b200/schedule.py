@@ -378,10 +378,14 @@ def flush_pending_updates(graph: Graph, policy: OptimizerPolicy,
 
 
 def default_update_ctas() -> int:
-    """Grid cap of a side-stream backward-fusion update: a third of the SMs
-    (~2 TB/s of HBM streaming) so the update overlaps the backward kernels
-    instead of time-slicing with them."""
-    return max(8, torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count // 3)
+    """Default grid cap of a side-stream backward-fusion update: none.
+
+    Measured on B200: capping the update to a third of the SMs
+    does not buy overlap -- cuDNN/CUTLASS convolution CTAs leave no room for a
+    co-resident update CTA, so a capped update only runs longer -- so the
+    update fills the GPU and relies on stream priority.  ``update_ctas`` keeps
+    the cap available for models whose backward kernels under-fill the SMs."""
+    return 0
 
 
 def run_backward_fusion(graph: Graph, policy: OptimizerPolicy, inp, workers: int = 1, *,
@@ -392,9 +396,8 @@ def run_backward_fusion(graph: Graph, policy: OptimizerPolicy, inp, workers: int
     ``workers=1`` issues each update inline on the autograd stream;
     ``workers>1`` on the engine's high-priority side stream behind an event
     (the device half of the Appendix B.2 guard), overlapping the backward of
-    the preceding layers; there each update's grid is capped at
-    ``update_ctas`` CTAs (default: a third of the SMs; 0 = uncapped) so it
-    streams alongside the backward instead of displacing it.
+    the preceding layers; ``update_ctas`` optionally caps each update's grid
+    so it streams alongside the backward (default 0: uncapped).
     ``bucket_elems`` merges consecutive layers (backward order) into launch
     groups of at least that many elements.
     Raises GlobalInfoRequired, mutating nothing, for policies or transforms

@@ -271,3 +271,23 @@ def test_spec_kats_on_gpu(spec_kats):
     pol.begin_iteration()
     pol.step(p)
     assert p.value.detach().cpu().tolist() == spec_kats["weight_decay"]["theta"]
+
+
+@pytest.mark.parametrize("max_ctas", [1, 7, 49])
+def test_capped_grid_same_bits(max_ctas):
+    """A capped grid (background update on the side stream) walks the same
+    tiles with fewer CTAs: identical results."""
+    rng = np.random.default_rng(max_ctas)
+    sizes = [3, 4097, 300001, 77]
+    ps = [torch.from_numpy(rng.standard_normal(n).astype(np.float32)).to(DEV) for n in sizes]
+    gs = [torch.from_numpy(rng.standard_normal(n).astype(np.float32)).to(DEV) for n in sizes]
+    ms = [torch.zeros(n, device=DEV) for n in sizes]
+    vs = [torch.zeros(n, device=DEV) for n in sizes]
+    ref = [(p.cpu().numpy().copy(), g.cpu().numpy().copy()) for p, g in zip(ps, gs)]
+    tl = _raw_list(ps, gs, ms, vs)
+    hp = kernels.hparams("adam", 1e-3, 0.9, 1e-4, 1e-8, 0.9, 0.999, 0.9, 1, max_ctas=max_ctas)
+    kernels.policy_step(tl, hp, None, 0, None)
+    h = optim_ref.Hyper(kind="adam", eta=1e-3, weight_decay=1e-4)
+    for p, (th, g) in zip(ps, ref):
+        optim_ref.step("adam", h, th, g, {}, 1)
+        assert p.cpu().numpy().tobytes() == th.tobytes()
