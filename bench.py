@@ -68,6 +68,8 @@ def parse_args(argv=None):
     ap.add_argument("--channels-last", type=int, default=1, help="1: NHWC model and inputs")
     ap.add_argument("--no-extras", action="store_true", help="headline only (for profilers)")
     ap.add_argument("--cpu-iters", type=int, default=2, help="CPU baseline sample iterations")
+    ap.add_argument("--instances", type=int, default=3,
+                    help="independently built model instances timed for the headline and key rows")
     return ap.parse_args(argv)
 
 
@@ -420,6 +422,10 @@ def _variants_c2(world: int):
     return v
 
 
+KEY_ROWS = ("torch.optim.SGD(foreach)", "ours:backward-fusion(w=2,bucket=256K)",
+            "ours:forward-fusion(bucket=256K)", "graph:torch.optim.SGD(foreach)",
+            "graph:ours:backward-fusion(w=2,bucket=256K)", "cl:graph:torch.optim.SGD(foreach)",
+            "cl:graph:ours:backward-fusion(w=2,bucket=256K)", "cl:graph:ours:forward-fusion(bucket=256K)")
 SWEEP_ROWS = ("torch.optim.SGD(foreach)", "ours:forward-fusion(bucket=256K)",
               "ours:backward-fusion(w=2,bucket=256K)", "graph:torch.optim.SGD(foreach)",
               "graph:ours:backward-fusion(w=2,bucket=256K)", "graph:ours:forward-fusion(bucket=256K)")
@@ -451,14 +457,23 @@ def run_ours(args) -> dict:
     flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=device)
     flush = flush_buf.zero_
 
-    step, g, pol = make_runner(args, args.batch, args.schedule, device)
-    n0 = _native.launch_count()
+    # cuDNN picks per model instance; timings are stable within an instance but
+    # differ by up to ~7% between instances (both arms), so the headline is the
+    # median over --instances independently built instances, each timed for
+    # exactly K steps after W warm-up steps.
+    inst = []
     with Clocks(dist.local) as clk:
-        ms = timed(step, args.steps, args.warmup, dist, flush)
-    if hasattr(step, "native_launches"):   # CUDA graph: kernel nodes replayed per step
-        launches = step.native_launches * args.steps
-    else:
-        launches = (_native.launch_count() - n0) * args.steps // (args.steps + args.warmup)
+        for _ in range(args.instances):
+            step, g, pol = make_runner(args, args.batch, args.schedule, device)
+            n0 = _native.launch_count()
+            inst.append(timed(step, args.steps, args.warmup, dist, flush))
+            if hasattr(step, "native_launches"):   # CUDA graph: kernel nodes replayed per step
+                launches = step.native_launches * args.steps
+            else:
+                launches = (_native.launch_count() - n0) * args.steps // (args.steps + args.warmup)
+            del step, g, pol
+            torch.cuda.empty_cache()
+    ms = statistics.median(inst)
     clocks = clk.summary()
     value = dist.world * args.batch * 1e3 / ms
     res = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": dist.world,
@@ -476,8 +491,7 @@ def run_ours(args) -> dict:
                                      f"default TF32 policy (allow_tf32={torch.backends.cudnn.allow_tf32}); "
                                      "optimizer update exact fp32 (reference arithmetic)")},
            "gpu_launches": int(launches)}
-    del step, g, pol
-    torch.cuda.empty_cache()
+    res["config"]["instances_ms_per_step"] = [round(t, 4) for t in inst]
     if not args.no_extras:
         sched = {}
         for b in [args.batch] + [int(x) for x in args.sweep.split(",") if x.strip()]:
@@ -485,12 +499,17 @@ def run_ours(args) -> dict:
             for name, sch, w, gr, opt, be, gph, cl in _variants_c2(dist.world):
                 if b != args.batch and name not in SWEEP_ROWS:
                     continue
-                st, *_ = make_runner(args, b, sch, device, workers=w, grad_reset=gr, opt_impl=opt,
-                                     bucket_elems=be, graphed=gph, channels_last=cl)
-                t = timed(st, args.steps, args.warmup, dist, flush)
+                ts = []
+                for _ in range(args.instances if name in KEY_ROWS else 1):
+                    st, *_ = make_runner(args, b, sch, device, workers=w, grad_reset=gr, opt_impl=opt,
+                                         bucket_elems=be, graphed=gph, channels_last=cl)
+                    ts.append(timed(st, args.steps, args.warmup, dist, flush))
+                    del st
+                    torch.cuda.empty_cache()
+                t = statistics.median(ts)
                 row[name] = {"ms_per_step": round(t, 4), "images_per_s": round(dist.world * b * 1e3 / t, 1)}
-                del st
-                torch.cuda.empty_cache()
+                if len(ts) > 1:
+                    row[name]["instances_ms"] = [round(x, 4) for x in ts]
             _speedups(row)
             sched[str(b)] = row
         res["schedules"] = sched

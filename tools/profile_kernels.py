@@ -16,22 +16,26 @@ from paper_2104_00237_b200.models import synthetic_batch  # noqa: E402
 
 
 def bf(iters=6):
-    g = of.build_classifier("mobilenet_v2_cifar", device="cuda")
+    g = of.build_classifier("mobilenet_v2_cifar", device="cuda", channels_last=True)
     g.track_counts = False
     pol = of.OptimizerPolicy("sgd-momentum", eta=0.1, alpha=0.9, weight_decay=5e-4, grad_reset="none")
     x, y = synthetic_batch("mobilenet_v2_cifar", 128, device="cuda")
+    x = x.contiguous(memory_format=torch.channels_last)
     for _ in range(iters):
-        of.run_backward_fusion(g, pol, (x, y), workers=2, bucket_elems=1 << 18, timing=False)
+        of.run_backward_fusion(g, pol, (x, y), workers=2, bucket_elems=1 << 18, timing=False)  # headline groups
     torch.cuda.synchronize()
 
 
 def vgg(iters=3):
     g = of.build_classifier("vgg16", device="cuda")
-    pol = of.OptimizerPolicy("adam", eta=1e-4)
+    pol = of.OptimizerPolicy("adam", eta=1e-4, grad_reset="none")
     for p in g.parameters:
         p.value.grad = torch.randn_like(p.value) * 0.01
     for _ in range(iters):
         pol.begin_iteration()
+        for p in g.parameters:
+            if p.value.grad is None:
+                p.value.grad = torch.randn_like(p.value) * 0.01
         pol.step_params(g.parameters)
     torch.cuda.synchronize()
 
