@@ -180,6 +180,7 @@ def timed(step, steps: int, warmup: int, dist: Dist, flush=None) -> float:
     dist.barrier()
     s = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.nvtx.range_push("timed")   # ncu --nvtx --nvtx-include timed/ selects this region
     e0.record(s)
     for _ in range(steps):
         if flush is not None:
@@ -187,6 +188,7 @@ def timed(step, steps: int, warmup: int, dist: Dist, flush=None) -> float:
         step()
     e1.record(s)
     torch.cuda.synchronize()
+    torch.cuda.nvtx.range_pop()
     dist.barrier()
     return dist.max(e0.elapsed_time(e1)) / steps
 

@@ -8,8 +8,8 @@ timeout 900 python bench.py ${BENCH_ARGS} > gpurun_out/bench.log 2>&1; echo benc
 tail -c 600 gpurun_out/bench.log
 if [ -n "${NCU}" ]; then
   # launch list of the headline command (skip the first 3000 launches: build, cudnn autotune, capture)
-  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 3000 -c 3000 --csv \
-    --log-file gpurun_out/launches.csv python bench.py --no-extras --steps 6 --warmup 3 > gpurun_out/ncu_bench.log 2>&1; echo ncu_list=$?
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "timed/" -c 3000 --csv \
+    --log-file gpurun_out/launches.csv python bench.py --no-extras --steps 4 --warmup 3 --instances 1 > gpurun_out/ncu_bench.log 2>&1; echo ncu_list=$?
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:mt_step -s 40 -c 3 \
     -o gpurun_out/prof_bf -f python tools/profile_kernels.py bf > gpurun_out/ncu_bf.log 2>&1; echo ncu_bf=$?
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:mt_step -s 1 -c 1 \
