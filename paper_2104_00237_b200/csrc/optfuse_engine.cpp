@@ -95,6 +95,7 @@ class Engine : public std::enable_shared_from_this<Engine> {
     const int np = static_cast<int>(params_.size());
     s0_.assign(np, at::Tensor());
     s1_.assign(np, at::Tensor());
+    master_.assign(np, at::Tensor());
     group_of_.assign(np, -1);
     pending_.assign(np, 0);
     updated_.assign(np, 0);
@@ -126,9 +127,14 @@ class Engine : public std::enable_shared_from_this<Engine> {
   }
 
   // -- configuration -------------------------------------------------------
-  void set_slots(int idx, c10::optional<at::Tensor> a, c10::optional<at::Tensor> b) {
+  // History slots of parameter idx and, for mixed precision, its fp32 master
+  // copy: the kernel then updates the master and writes the (bf16) parameter
+  // as the shadow in the same pass.
+  void set_slots(int idx, c10::optional<at::Tensor> a, c10::optional<at::Tensor> b,
+                 c10::optional<at::Tensor> master) {
     s0_.at(idx) = a.has_value() ? *a : at::Tensor();
     s1_.at(idx) = b.has_value() ? *b : at::Tensor();
+    master_.at(idx) = master.has_value() ? *master : at::Tensor();
     // static pointers of the BF groups
     const int gi = group_of_[idx];
     if (gi >= 0) refresh_static(groups_[gi]);
@@ -313,13 +319,16 @@ class Engine : public std::enable_shared_from_this<Engine> {
   void refresh_static(Group& G) {
     for (size_t k = 0; k < G.members.size(); ++k) {
       const int idx = G.members[k];
-      G.p[k] = params_[idx].data_ptr();
+      const bool mixed = master_[idx].defined();
+      G.p[k] = mixed ? master_[idx].data_ptr() : params_[idx].data_ptr();
       G.s0[k] = s0_[idx].defined() ? s0_[idx].data_ptr() : nullptr;
       G.s1[k] = s1_[idx].defined() ? s1_[idx].data_ptr() : nullptr;
-      G.sh[k] = nullptr;
+      G.sh[k] = mixed ? params_[idx].data_ptr() : nullptr;
       G.n[k] = params_[idx].numel();
     }
-    G.list.param_dtype = dtype_code(params_[G.members[0]].scalar_type());
+    const int first = G.members[0];
+    G.list.param_dtype = dtype_code(master_[first].defined() ? master_[first].scalar_type()
+                                                              : params_[first].scalar_type());
   }
 
   // Fills the grad pointers (allocating a zero gradient on the current stream
@@ -392,7 +401,7 @@ class Engine : public std::enable_shared_from_this<Engine> {
     prof_.clear();
   }
 
-  std::vector<at::Tensor> params_, s0_, s1_;
+  std::vector<at::Tensor> params_, s0_, s1_, master_;
   std::vector<std::vector<int>> layers_;
   std::vector<std::vector<int>> ff_units_;
   std::vector<Group> groups_;

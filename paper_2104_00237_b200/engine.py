@@ -79,10 +79,11 @@ class FusionEngine:
                                [[p.id for p in L.params] for L in graph.layers],
                                self.stream.cuda_stream if self.stream is not None else 0)
         slots = policy.history_slots()
+        self.mixed = graph.master_weights
         for p in params:
             a = p.history[slots[0]] if slots else None
             b = p.history[slots[1]] if len(slots) > 1 else None
-            self.native.set_slots(p.id, a, b)
+            self.native.set_slots(p.id, a, b, p.master)
         self._hp_key = None
         self.ff_bucket_elems = 0
         self.ff_leaders = None
@@ -97,10 +98,10 @@ class FusionEngine:
         hp = kernels.hparams(policy.kind, policy.eta, policy.alpha, policy.weight_decay,
                              policy.epsilon, policy.beta1, policy.beta2, policy.rho, step_t)
         zero = policy.grad_reset == "zero"
+        flags = (nat.OF_FLAG_ZERO_GRAD if zero else 0) | (nat.OF_FLAG_SHADOW_BF16 if self.mixed else 0)
         self.native.set_hparams(hp.kind, hp.eta, hp.alpha, hp.weight_decay, hp.epsilon, hp.beta1,
                                 hp.beta2, hp.rho, hp.bias_correction1, hp.bias_correction2,
-                                nat.OF_FLAG_ZERO_GRAD if zero else 0, not zero, grad_scale,
-                                max_ctas)
+                                flags, not zero, grad_scale, max_ctas)
         self._hp_key = key
 
     @property

@@ -27,7 +27,7 @@ from __future__ import annotations
 import torch
 
 from . import trace as tr
-from .errors import StateError
+from .errors import ConfigError, StateError
 
 
 class Parameter:
@@ -38,7 +38,7 @@ class Parameter:
     """
 
     __slots__ = ("id", "name", "value", "history", "count", "_updated", "_pending",
-                 "_grad_scale", "_layout_ok", "layers", "_flags")
+                 "_grad_scale", "_layout_ok", "layers", "_flags", "master")
 
     def __init__(self, pid: int, value: torch.Tensor, name: str = ""):
         self.id = pid
@@ -52,6 +52,7 @@ class Parameter:
         self._layout_ok = False
         self.layers: list = []
         self._flags = None
+        self.master = None   # fp32 master copy when the model runs in bf16
 
     @property
     def pending(self) -> bool:
@@ -152,9 +153,35 @@ class Graph:
         self._engines: dict = {}      # native fusion engines, by configuration
         self._flag_owner = None       # engine holding the pending/updated flags
         self._hook_owner = None       # engine whose C++ hooks sit on the parameters
+        self.master_weights = False
         self._pre_handles = None
         self._leader_handles = None   # bucketed forward fusion: hooks on bucket leaders only
         self.exec_order = None        # layer indices in first-execution order (recorded)
+
+    # -- mixed precision -------------------------------------------------------
+
+    def use_master_weights(self, dtype=torch.bfloat16) -> None:
+        """Run the module in ``dtype`` (bf16) and keep fp32 master weights.
+
+        Every parameter gets an fp32 ``master`` copy taken from its current
+        value; the module (parameters and buffers) is cast to ``dtype``.  The
+        update kernels then read the bf16 gradient, update the fp32 master and
+        history, and write the bf16 parameter back in the same pass
+        (OF_FLAG_SHADOW_BF16: 2+4+8 B read, 4+8+2 B written per element).
+        Must be called before any optimizer state exists."""
+        if dtype != torch.bfloat16:
+            raise ConfigError("master weights are supported for bfloat16 models")
+        if self._engines or any(p.history for p in self.parameters):
+            raise StateError("use_master_weights must precede the first update")
+        for p in self.parameters:
+            if p.value.dtype != torch.float32:
+                raise ConfigError(f"parameter {p.id} is {p.value.dtype}; masters start from float32")
+            p.master = p.value.detach().clone()
+        self.module.to(dtype)
+        for p in self.parameters:
+            p.value.grad = None
+            p._layout_ok = False
+        self.master_weights = True
 
     # -- structure ---------------------------------------------------------
 

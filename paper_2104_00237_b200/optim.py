@@ -154,14 +154,18 @@ class OptimizerPolicy:
         self.prepare(params)
         s_a = slots[0] if slots else None
         s_b = slots[1] if len(slots) > 1 else None
+        mixed = params[0].master is not None
         for i, p in enumerate(params):
             v = p.value
             h = p.history
-            tl.set(i, v, v.grad, h[s_a] if s_a else None, h[s_b] if s_b else None, None)
-        p0 = params[0].value
-        tl.set_dtypes(p0.dtype, p0.grad.dtype)
-        kernels.policy_step(tl, self._hparams(t), scale,
-                            nat.OF_FLAG_ZERO_GRAD if zero else 0, stream)
+            if mixed:   # fp32 master updated, bf16 parameter written as the shadow
+                tl.set(i, p.master, v.grad, h[s_a] if s_a else None, h[s_b] if s_b else None, v)
+            else:
+                tl.set(i, v, v.grad, h[s_a] if s_a else None, h[s_b] if s_b else None, None)
+        p0 = params[0]
+        tl.set_dtypes(p0.master.dtype if mixed else p0.value.dtype, p0.value.grad.dtype)
+        flags = (nat.OF_FLAG_ZERO_GRAD if zero else 0) | (nat.OF_FLAG_SHADOW_BF16 if mixed else 0)
+        kernels.policy_step(tl, self._hparams(t), scale, flags, stream)
         if trace is not None:
             for p in params:
                 trace.record_mem(tr.PARAM, p.id, tr.READ)
@@ -196,9 +200,10 @@ class OptimizerPolicy:
         for p in params:
             h = p.history
             if len(h) < len(slots):
+                ref = p.master if p.master is not None else p.value
                 for name in slots:
                     if name not in h:
-                        h[name] = torch.zeros_like(p.value, memory_format=torch.preserve_format)
+                        h[name] = torch.zeros_like(ref, memory_format=torch.preserve_format)
 
     def _hparams(self, t: int) -> nat.OfHparams:
         key = (t, self.kind, self.eta, self.alpha, self.weight_decay, self.epsilon,
@@ -224,19 +229,29 @@ def bytes_per_element(kind: str, param_itemsize: int = 4, grad_itemsize: int | N
 def algorithmic_bytes(kind: str, params) -> int:
     total = 0
     for p in params:
-        v = p.value if hasattr(p, "value") else p
-        total += v.numel() * bytes_per_element(kind, v.element_size())
+        if hasattr(p, "value"):
+            total += p.value.numel() * bytes_per_element_of(kind, p)
+        else:
+            total += p.numel() * bytes_per_element(kind, p.element_size())
     return total
 
 
 def _check_layout(p, g) -> None:
-    """Parameter, gradient and (zeros_like) history must share one dense
-    layout: the kernels walk the three buffers in storage order."""
+    """Parameter, gradient, history (and master) must share one dense layout:
+    the kernels walk the buffers in storage order."""
     v = p.value
     if not v.is_cuda:
         raise ConfigError(f"parameter {p.id} is on {v.device}; the update kernels run on CUDA only")
-    if v.dtype not in (torch.float32, torch.float64):
-        raise ConfigError(f"parameter {p.id} has dtype {v.dtype}; expected float32 or float64")
+    m = p.master
+    if m is not None:
+        if v.dtype != torch.bfloat16 or m.dtype != torch.float32:
+            raise ConfigError(f"parameter {p.id}: master weights need a bf16 parameter and an "
+                              f"fp32 master, got {v.dtype} / {m.dtype}")
+        if m.shape != v.shape or m.stride() != v.stride() or m.device != v.device:
+            raise ConfigError(f"parameter {p.id}: master layout differs from the parameter's")
+    elif v.dtype not in (torch.float32, torch.float64):
+        raise ConfigError(f"parameter {p.id} has dtype {v.dtype}; expected float32 or float64 "
+                          "(or bf16 with master weights)")
     if not (v.is_contiguous() or v.is_contiguous(memory_format=torch.channels_last)):
         raise ConfigError(f"parameter {p.id} is not dense; the update kernels need dense storage")
     if g is None:
@@ -244,9 +259,17 @@ def _check_layout(p, g) -> None:
     if g.shape != v.shape or g.stride() != v.stride() or g.device != v.device:
         raise ConfigError(f"parameter {p.id}: gradient layout {tuple(g.stride())} on {g.device} "
                           f"differs from parameter layout {tuple(v.stride())} on {v.device}")
-    if not (g.dtype == v.dtype or (g.dtype == torch.bfloat16 and v.dtype == torch.float32)):
+    if g.dtype != v.dtype:
         raise ConfigError(f"parameter {p.id}: gradient dtype {g.dtype} with parameter {v.dtype}")
     p._layout_ok = True
+
+
+def bytes_per_element_of(kind: str, p) -> int:
+    """Algorithmic bytes per element for this parameter's storage (mixed: bf16
+    grad in, fp32 master + history, bf16 shadow out)."""
+    if p.master is not None:
+        return bytes_per_element(kind, 4, 2, shadow=True)
+    return bytes_per_element(kind, p.value.element_size())
 
 
 def clip_factor(graph, max_norm: float, trace: tr.ScheduleTrace | None = None, stream=None):
