@@ -337,7 +337,7 @@ def measure_update_kernel(args, device, peaks) -> dict:
         gbs = nbytes / t / 1e9
         out[name] = {"bytes": nbytes, "us": t * 1e6, "achieved_gbs": round(gbs, 1),
                      "frac": round(gbs / peaks["hbm_gbs"], 4), "tensors": len(params),
-                     "launches": (len(params) + 63) // 64}
+                     "launches": (len(params) + 255) // 256}
         del g, params
         torch.cuda.empty_cache()
     return out

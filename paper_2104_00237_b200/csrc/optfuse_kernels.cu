@@ -37,6 +37,7 @@ constexpr int kVec = 4;
 constexpr int kUnroll = 4;
 constexpr int kTile = kThreads * kVec * kUnroll;  // elements per tile
 constexpr int kCtasPerSm = 8;
+constexpr int kCapMax = 256;                      // tensors per launch (param block)
 constexpr int kSqnormWorkspace = 148 * 8 * 4;      // >= any sqnorm grid we launch
 
 std::atomic<uint64_t> g_launches{0};
@@ -213,6 +214,20 @@ struct MTParams {
   int32_t count;
 };
 
+// Index of the tensor owning `tile`: binary search over the inclusive tile
+// prefix sum, starting at `from` (tiles visited by one CTA only increase).
+// With up to 256 tensors per launch a linear scan from 0 would cost a CTA
+// hundreds of dependent parameter-bank loads before its first byte moves.
+template <int CAP>
+__device__ __forceinline__ int find_tensor(const MTParams<CAP>& mp, int from, int tile) {
+  int lo = from, hi = mp.count - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (tile < mp.tile_end[mid]) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+
 // 4-element vector loads/stores.
 __device__ __forceinline__ void ld4(const float* p, float (&v)[4]) {
   const float4 t = *reinterpret_cast<const float4*>(p);
@@ -285,7 +300,7 @@ mt_step_kernel(const __grid_constant__ MTParams<CAP> mp, const Op op,
   const T scale = has_scale ? T(*gscale) : T(1);
   int ti = 0;
   for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-    while (tile >= mp.tile_end[ti]) ++ti;
+    ti = find_tensor(mp, ti, tile);
     const int tfirst = ti ? mp.tile_end[ti - 1] : 0;
     const int64_t base = static_cast<int64_t>(tile - tfirst) * kTileU;
     const int64_t rem = mp.n[ti] - base;
@@ -359,7 +374,7 @@ mt_sqnorm_kernel(const __grid_constant__ MTParams<CAP> mp, double* __restrict__ 
   double acc = 0.0;
   int ti = 0;
   for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-    while (tile >= mp.tile_end[ti]) ++ti;
+    ti = find_tensor(mp, ti, tile);
     const int tfirst = ti ? mp.tile_end[ti - 1] : 0;
     const int64_t base = static_cast<int64_t>(tile - tfirst) * kTile;
     const int64_t rem = mp.n[ti] - base;
@@ -500,9 +515,14 @@ int launch_step(const of_tensor_list* l, const Op& op, const float* gscale, uint
     } else if (left <= 16) {
       st = launch_step_chunk<Op, T, G, 16>(l, first, left, op, gscale, flags, max_ctas, s);
       first += left;
+    } else if (left <= 64) {
+      st = launch_step_chunk<Op, T, G, 64>(l, first, left, op, gscale, flags, max_ctas, s);
+      first += left;
     } else {
-      const int c = left < 64 ? left : 64;
-      st = launch_step_chunk<Op, T, G, 64>(l, first, c, op, gscale, flags, max_ctas, s);
+      // up to 256 tensors in one launch: a 13 KB parameter block (CUDA >= 12.1
+      // accepts up to 32 KB), so a whole CNN's parameter set is one kernel
+      const int c = left < kCapMax ? left : kCapMax;
+      st = launch_step_chunk<Op, T, G, kCapMax>(l, first, c, op, gscale, flags, max_ctas, s);
       first += c;
     }
     if (st != OF_OK) return st;
@@ -591,8 +611,8 @@ int launch_sqnorm(const of_tensor_list* l, double* ws, int64_t ws_len, double* o
   int first = 0;
   do {
     const int left = l->n - first;
-    const int c = left < 64 ? left : 64;
-    const int st = launch_sqnorm_chunk<G, 64>(l, first, c, ws, ws_len, out, accumulate, s);
+    const int c = left < kCapMax ? left : kCapMax;
+    const int st = launch_sqnorm_chunk<G, kCapMax>(l, first, c, ws, ws_len, out, accumulate, s);
     if (st != OF_OK) return st;
     accumulate = 1;
     first += c;

@@ -28,6 +28,7 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
+from . import _native as nat
 from . import kernels
 from .engine import launch_groups
 from .errors import ConfigError, GlobalInfoRequired, StateError
@@ -37,7 +38,7 @@ DEFAULT_BUCKET_ELEMS = 1 << 22  # 16 MiB of fp32 per bucket
 
 class _Bucket:
     __slots__ = ("index", "params", "flat_param", "flat_grad", "grad_shard", "slots", "shard",
-                 "tl", "ready", "event", "done", "leader", "pending")
+                 "master", "tl", "ready", "event", "done", "leader", "pending")
 
     def __init__(self, index):
         self.index = index
@@ -66,6 +67,14 @@ class DataParallelFusion:
             raise ConfigError("the sharded update runs on CUDA; pass update_fn only for host tests")
         self.comm = torch.cuda.Stream() if self.cuda else None
         slots = policy.history_slots()
+        # mixed precision (C4): the module runs in bf16 with fp32 masters
+        # (Graph.use_master_weights).  Gradients are reduce-scattered in bf16;
+        # rank r keeps the fp32 master and history of its shard only; the
+        # kernel writes the updated bf16 parameters straight into the shard of
+        # flat_param (OF_FLAG_SHADOW_BF16) and only bf16 is all-gathered.
+        self.mixed = bool(getattr(graph, "master_weights", False))
+        self.flags = nat.OF_FLAG_SHADOW_BF16 if self.mixed else 0
+        src = dist.get_global_rank(group, 0) if group else 0
         unit = self.world * 4
         self.buckets = []
         for bi, ids in enumerate(launch_groups(graph, bucket_elems)):
@@ -74,11 +83,15 @@ class DataParallelFusion:
             dt = b.params[0].value.dtype
             if any(p.value.dtype != dt for p in b.params):
                 raise ConfigError("a data-parallel bucket needs one dtype")
+            if self.mixed and any(p.master is None for p in b.params):
+                raise ConfigError("master weights: every parameter needs an fp32 master")
+            mdt = torch.float32 if self.mixed else dt
             n = sum(p.value.numel() for p in b.params)
             padded = -(-n // unit) * unit
             S = padded // self.world
             b.flat_param = torch.zeros(padded, dtype=dt, device=self.device)
             b.flat_grad = torch.zeros(padded, dtype=dt, device=self.device)
+            flat_master = torch.zeros(padded, dtype=mdt, device=self.device) if self.mixed else None
             off = 0
             with torch.no_grad():
                 for p in b.params:
@@ -87,26 +100,44 @@ class DataParallelFusion:
                         raise ConfigError(f"parameter {p.id} must be contiguous for data parallel")
                     k = v.numel()
                     b.flat_param[off:off + k].copy_(v.reshape(-1))
+                    if self.mixed:
+                        flat_master[off:off + k].copy_(p.master.reshape(-1))
                     v.data = b.flat_param[off:off + k].view_as(v)
                     v.grad = b.flat_grad[off:off + k].view_as(v)
                     off += k
-            dist.broadcast(b.flat_param, src=dist.get_global_rank(group, 0) if group else 0,
-                           group=group)
+            if self.mixed:
+                dist.broadcast(flat_master, src=src, group=group)
+                with torch.no_grad():
+                    b.flat_param.copy_(flat_master)
+            else:
+                dist.broadcast(b.flat_param, src=src, group=group)
             b.shard = slice(self.rank * S, (self.rank + 1) * S)
             b.grad_shard = torch.zeros(S, dtype=dt, device=self.device)
-            b.slots = {name: torch.zeros(S, dtype=dt, device=self.device) for name in slots}
+            b.slots = {name: torch.zeros(S, dtype=mdt, device=self.device) for name in slots}
+            # the owned fp32 master shard (state memory / W); the full-size
+            # per-parameter masters are released: a non-DP schedule on this
+            # graph now fails loudly instead of updating stale masters
+            b.master = flat_master[b.shard].clone() if self.mixed else None
+            del flat_master
             if self.cuda:
                 tl = kernels.TensorList(1)
                 pv = b.flat_param[b.shard]
-                tl.set(0, pv, b.grad_shard, b.slots[slots[0]] if slots else None,
-                       b.slots[slots[1]] if len(slots) > 1 else None)
-                tl.set_dtypes(dt, dt)
+                if self.mixed:
+                    tl.set(0, b.master, b.grad_shard, b.slots[slots[0]] if slots else None,
+                           b.slots[slots[1]] if len(slots) > 1 else None, pv)
+                else:
+                    tl.set(0, pv, b.grad_shard, b.slots[slots[0]] if slots else None,
+                           b.slots[slots[1]] if len(slots) > 1 else None)
+                tl.set_dtypes(mdt, dt)
                 b.tl = tl
                 b.event = torch.cuda.Event()
                 b.done = torch.cuda.Event()
             b.ready = 0
             b.pending = False
             self.buckets.append(b)
+        if self.mixed:
+            for p in graph.parameters:
+                p.master = None
         self.bucket_of = {p.id: b for b in self.buckets for p in b.params}
         self.scale = None
         if self.cuda:
@@ -124,10 +155,16 @@ class DataParallelFusion:
 
     def _update_and_gather(self, b, t: int) -> None:
         if self.update_fn is not None:
-            b.grad_shard.mul_(1.0 / self.world)
-            self.update_fn(b.flat_param[b.shard], b.grad_shard, b.slots, t)
+            if self.mixed:    # host stand-in: fp32 grad shard, master updated, bf16 written back
+                g = b.grad_shard.float().mul_(1.0 / self.world)
+                self.update_fn(b.master, g, b.slots, t)
+                with torch.no_grad():
+                    b.flat_param[b.shard].copy_(b.master)
+            else:
+                b.grad_shard.mul_(1.0 / self.world)
+                self.update_fn(b.flat_param[b.shard], b.grad_shard, b.slots, t)
         else:
-            kernels.policy_step(b.tl, self.policy._hparams(t), self.scale, 0, None)
+            kernels.policy_step(b.tl, self.policy._hparams(t), self.scale, self.flags, None)
         dist.all_gather_into_tensor(b.flat_param, b.flat_param[b.shard], group=self.group)
 
     def _on_stream(self, stream):

@@ -96,3 +96,80 @@ def test_sharded_update_equals_single_process(schedule):
     got = np.frombuffer(out[0], np.float32)
     ref = np.frombuffer(want, np.float32)
     assert got.tobytes() == ref.tobytes(), np.abs(got - ref).max()
+
+
+# -- mixed precision (C4): bf16 module, fp32 master shards, bf16 all-gather --
+
+def _worker_mixed(rank, world, port, schedule, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2104_00237_b200 as of
+        from paper_2104_00237_b200.dp import DataParallelFusion
+        g = of.build_model("shared-chain", layers=4, width=6, device="cpu", exact=False,
+                           track_input_grad=False)
+        g.use_master_weights()
+        pol = of.OptimizerPolicy(KIND, eta=ETA, weight_decay=WD)
+        dp = DataParallelFusion(g, pol, bucket_elems=40, update_fn=_oracle_update)
+        assert dp.mixed and all(p.master is None for p in g.parameters)
+        assert all(b.master.dtype == torch.float32 and b.flat_param.dtype == torch.bfloat16
+                   for b in dp.buckets)
+        run = {"backward-fusion": dp.run_backward_fusion, "baseline": dp.run_baseline,
+               "forward-fusion": dp.run_forward_fusion}[schedule]
+        for x in _inputs(rank):
+            run(x.to(torch.bfloat16))
+        dp.flush()
+        flat = torch.cat([p.value.detach().reshape(-1) for p in g.parameters])
+        shards = [(b.master.numpy().copy(), [p.id for p in b.params]) for b in dp.buckets]
+        out[rank] = (flat.view(torch.int16).numpy().tobytes(), shards)
+    finally:
+        dist.destroy_process_group()
+
+
+def _single_process_mixed():
+    """One process, both ranks' bf16 gradients summed in bf16 (the reduce-
+    scatter), averaged in fp32, fp32 master updated by the reference rule, bf16
+    parameter = round(master)."""
+    import paper_2104_00237_b200 as of
+    from oracle import optim_ref
+    g = of.build_model("shared-chain", layers=4, width=6, device="cpu", exact=False,
+                       track_input_grad=False)
+    masters = [p.value.detach().reshape(-1).clone().numpy() for p in g.parameters]
+    g.module.to(torch.bfloat16)
+    hp = optim_ref.Hyper(kind=KIND, eta=ETA, weight_decay=WD)
+    slots = [dict() for _ in g.parameters]
+    xs = [_inputs(r) for r in range(2)]
+    for it in range(ITERS):
+        grads = []
+        for r in range(2):
+            for p in g.parameters:
+                p.value.grad = None
+            g.module(xs[r][it].to(torch.bfloat16)).float().backward()
+            grads.append([p.value.grad.reshape(-1).clone() for p in g.parameters])
+        for k, p in enumerate(g.parameters):
+            avg = ((grads[0][k] + grads[1][k]).float() * 0.5).numpy()
+            optim_ref.step(KIND, hp, masters[k], avg, slots[k], it + 1)
+            with torch.no_grad():
+                p.value.copy_(torch.from_numpy(masters[k]).view_as(p.value))
+    flat = torch.cat([p.value.detach().reshape(-1) for p in g.parameters])
+    return flat.view(torch.int16).numpy().tobytes(), masters
+
+
+@pytest.mark.parametrize("schedule", ["backward-fusion", "forward-fusion"])
+def test_sharded_mixed_precision_equals_single_process(schedule):
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().dict()
+    mp.start_processes(_worker_mixed, args=(2, _free_port(), schedule, out), nprocs=2, join=True,
+                       start_method="spawn")
+    assert out[0][0] == out[1][0], "ranks disagree on the bf16 parameters after the all-gather"
+    want_bf16, want_master = _single_process_mixed()
+    assert out[0][0] == want_bf16
+    # each rank owns one shard of every bucket's fp32 master: stitch rank 0 +
+    # rank 1 per bucket and compare with the reference masters bit for bit
+    for (s0, ids), (s1, ids1) in zip(out[0][1], out[1][1]):
+        assert ids == ids1
+        full = np.concatenate([s0, s1])
+        want = np.concatenate([want_master[i] for i in ids])
+        assert full[:want.size].tobytes() == want.tobytes()
+        assert not full[want.size:].any()     # padding stays zero
