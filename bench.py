@@ -67,6 +67,8 @@ def parse_args(argv=None):
                     help="1: capture each iteration (ours and the torch baseline) as a CUDA graph")
     ap.add_argument("--channels-last", type=int, default=1, help="1: NHWC model and inputs")
     ap.add_argument("--no-extras", action="store_true", help="headline only (for profilers)")
+    ap.add_argument("--extras", default="c1,c3,c4,c5",
+                    help="other BASELINE.json configs timed beside the headline ('' to skip)")
     ap.add_argument("--cpu-iters", type=int, default=2, help="CPU baseline sample iterations")
     ap.add_argument("--instances", type=int, default=3,
                     help="independently built model instances timed for the headline and key rows")
@@ -205,14 +207,31 @@ def load_peaks() -> dict:
 # our arm
 # ---------------------------------------------------------------------------
 
-# BASELINE.json configs measured here: C2 (the headline) and C3 (update-bound)
+# BASELINE.json configs measured here: C2 (the headline) plus C1, C3, C4, C5 as
+# single-GPU extras (their multi-GPU data-parallel form runs under torchrun)
 WORKLOADS = {
+    "c1": {"model": "resnet18_cifar", "batch": 128, "kind": "sgd-momentum",
+           "hp": {"eta": 0.1, "alpha": 0.9, "weight_decay": 5e-4},
+           "torch": ("SGD", {"lr": 0.1, "momentum": 0.9, "weight_decay": 5e-4}),
+           "desc": "ResNet-18 (CIFAR stem) on synthetic 3x32x32, batch 128, SGD-momentum, fp32"},
     "c2": {"model": "mobilenet_v2_cifar", "batch": 128, "kind": "sgd-momentum",
            "hp": {"eta": 0.1, "alpha": 0.9, "weight_decay": 5e-4},
            "torch": ("SGD", {"lr": 0.1, "momentum": 0.9, "weight_decay": 5e-4})},
     "c3": {"model": "vgg16", "batch": 32, "kind": "adam",
            "hp": {"eta": 1e-4, "weight_decay": 1e-4},
-           "torch": ("Adam", {"lr": 1e-4, "weight_decay": 1e-4})},
+           "torch": ("Adam", {"lr": 1e-4, "weight_decay": 1e-4}),
+           "desc": "VGG-16 on synthetic 3x224x224, batch 32, Adam (coupled wd 1e-4), fp32"},
+    "c4": {"model": "resnet50", "batch": 64, "kind": "adamw", "mixed": True,
+           "hp": {"eta": 1e-3, "weight_decay": 0.05},
+           "torch": ("AdamW", {"lr": 1e-3, "weight_decay": 0.05}),
+           "desc": ("ResNet-50 on synthetic 3x224x224, batch 64, AdamW (wd 0.05); ours: bf16 model "
+                    "with fp32 master weights updated in one pass (bf16 grad in, bf16 param out); "
+                    "torch: fp32 params under torch.autocast(bf16)")},
+    "c5": {"model": "bert_base", "batch": 32, "kind": "adamw",
+           "hp": {"eta": 1e-4, "weight_decay": 0.01},
+           "torch": ("AdamW", {"lr": 1e-4, "weight_decay": 0.01}),
+           "desc": ("BERT-base pre-training (BertForPreTraining, random init), seq 128, batch 32, "
+                    "15% MLM labels + NSP, AdamW (wd 0.01), fp32 (TF32 matmuls)")},
 }
 
 
@@ -220,45 +239,62 @@ def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
                 grad_reset=None, opt_impl=None, bucket_elems=None, graphed=None,
                 workload="c2", channels_last=None):
     """Returns (step_fn, graph_or_model, policy_or_opt).  ``opt_impl`` selects
-    the unfused torch.optim baseline ("foreach" | "fused"); ``graphed``
-    captures the whole iteration as a CUDA graph (paper_2104_00237_b200.graphs)."""
+    the unfused torch.optim baseline ("foreach" | "fused") or "none" (forward
+    + backward only, no update: the lower bound any fusion can reach);
+    ``graphed`` captures the whole iteration as a CUDA graph
+    (paper_2104_00237_b200.graphs)."""
     import torch
-    import torch.nn.functional as F
 
     import paper_2104_00237_b200 as of
     from paper_2104_00237_b200.graphs import CapturedStep
     from paper_2104_00237_b200.models import synthetic_batch
 
     wl = WORKLOADS[workload]
+    mixed = wl.get("mixed", False)
     graphed = args.graphs if graphed is None else graphed
     cl = args.channels_last if channels_last is None else channels_last
     x, y = synthetic_batch(wl["model"], batch, device=device, seed=seed)
-    if cl:
+    if cl and x.dim() == 4:
         x = x.contiguous(memory_format=torch.channels_last)
     world = getattr(args, "world", 1)
-    if opt_impl is not None:  # unfused torch.optim baseline
+    if opt_impl is not None:  # unfused torch.optim baseline (or no update at all)
         g = of.build_classifier(wl["model"], device=device, seed=seed, channels_last=bool(cl))
-        net = g.module  # plain module: the Graph installs no hooks until a schedule runs
+        net, loss_fn = g.module, g.loss_fn  # plain module: no hooks until a schedule runs
         name, kw = wl["torch"]
-        kw = dict(kw, **({"foreach": True} if opt_impl == "foreach" else {"fused": True}))
-        if graphed and name == "Adam":
-            kw["capturable"] = True
-        opt = getattr(torch.optim, name)(net.parameters(), **kw)
+        opt = None
+        if opt_impl != "none":
+            kw = dict(kw, **({"foreach": True} if opt_impl == "foreach" else {"fused": True}))
+            if graphed and name in ("Adam", "AdamW"):
+                kw["capturable"] = True
+            opt = getattr(torch.optim, name)(net.parameters(), **kw)
         if world > 1:  # unfused data parallel: DDP all-reduce + torch.optim
             net = torch.nn.parallel.DistributedDataParallel(net, device_ids=[device.index])
             graphed = False
+        amp = torch.autocast("cuda", dtype=torch.bfloat16) if mixed else None
 
         def run(inp):
-            opt.zero_grad(set_to_none=True)
-            loss = F.cross_entropy(net(inp[0]), inp[1])
+            if opt is not None:
+                opt.zero_grad(set_to_none=True)
+            else:
+                for p in net.parameters():
+                    p.grad = None
+            if amp is not None:
+                with amp:
+                    loss = loss_fn(net(inp[0]), inp[1])
+            else:
+                loss = loss_fn(net(inp[0]), inp[1])
             loss.backward()
-            opt.step()
+            if opt is not None:
+                opt.step()
             return loss
         owner, pol = net, opt
     elif world > 1:  # data parallel: sharded fused update over NCCL
         from paper_2104_00237_b200.dp import DataParallelFusion
         g = of.build_classifier(wl["model"], device=device, seed=seed)
         g.track_counts = False
+        if mixed:
+            g.use_master_weights()
+            x = x.to(torch.bfloat16) if x.is_floating_point() else x
         pol = of.OptimizerPolicy(wl["kind"], **wl["hp"])
         dpf = DataParallelFusion(g, pol)
         dp_run = {"baseline": dpf.run_baseline, "forward-fusion": dpf.run_forward_fusion,
@@ -271,6 +307,9 @@ def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
     else:
         g = of.build_classifier(wl["model"], device=device, seed=seed, channels_last=bool(cl))
         g.track_counts = False  # no per-layer Python pre-hooks unless a schedule needs them
+        if mixed:
+            g.use_master_weights()
+            x = x.to(torch.bfloat16) if x.is_floating_point() else x
         pol = of.OptimizerPolicy(wl["kind"], **wl["hp"], grad_reset=grad_reset or args.grad_reset)
         w = args.workers if workers is None else workers
         ctas = None
@@ -303,9 +342,11 @@ def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
 
 
 def measure_update_kernel(args, device, peaks) -> dict:
-    """Standalone roofline of the multi-tensor kernel: one launch over a whole
-    parameter set, L2 flushed before every launch (VGG-16 shapes with Adam --
-    the update-bound config C3 -- and the MobileNetV2 set with SGD-momentum)."""
+    """Standalone roofline of the multi-tensor kernel: one pass over a whole
+    parameter set (as few launches as the 256-tensor parameter block allows),
+    L2 flushed before every pass: VGG-16 with Adam (C3, update-bound),
+    BERT-base with AdamW (C5), ResNet-50 bf16 + fp32 masters with AdamW (C4:
+    bf16 grad in, bf16 parameter out) and MobileNetV2 with SGD-momentum (C2)."""
     import torch
 
     import paper_2104_00237_b200 as of
@@ -313,10 +354,14 @@ def measure_update_kernel(args, device, peaks) -> dict:
 
     out = {}
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=device)
-    for name, model, kind in (("vgg16_adam", "vgg16", "adam"),
-                              ("mobilenet_v2_sgdm", "mobilenet_v2_cifar", "sgd-momentum")):
+    for name, model, kind, mixed in (("vgg16_adam", "vgg16", "adam", False),
+                                     ("bert_base_adamw", "bert_base", "adamw", False),
+                                     ("resnet50_bf16_master_adamw", "resnet50", "adamw", True),
+                                     ("mobilenet_v2_sgdm", "mobilenet_v2_cifar", "sgd-momentum", False)):
         g = of.build_classifier(model, device=device)
-        pol = of.OptimizerPolicy(kind, eta=1e-4)
+        if mixed:
+            g.use_master_weights()
+        pol = of.OptimizerPolicy(kind, eta=1e-4, weight_decay=0.01 if kind == "adamw" else 0.0)
         params = g.parameters
         for p in params:
             p.value.grad = torch.randn_like(p.value) * 0.01
@@ -335,12 +380,21 @@ def measure_update_kernel(args, device, peaks) -> dict:
         nbytes = algorithmic_bytes(kind, params)
         t = statistics.median(times) / 1e3
         gbs = nbytes / t / 1e9
-        out[name] = {"bytes": nbytes, "us": t * 1e6, "achieved_gbs": round(gbs, 1),
+        out[name] = {"bytes": nbytes, "us": round(t * 1e6, 2), "achieved_gbs": round(gbs, 1),
                      "frac": round(gbs / peaks["hbm_gbs"], 4), "tensors": len(params),
                      "launches": (len(params) + 255) // 256}
         del g, params
         torch.cuda.empty_cache()
     return out
+
+
+def ncu_traffic(kernel: str) -> dict | None:
+    """DRAM bytes per launch of ``kernel`` from the committed ncu --set full
+    capture (profiles/ncu_traffic.json, written by tools/summarize_ncu.py)."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if not p.exists():
+        return None
+    return json.loads(p.read_text()).get(kernel)
 
 
 def measure_in_situ(args, device, peaks, reps: int = 5) -> dict:
@@ -394,7 +448,11 @@ def cpu_baseline(args, iters: int) -> dict:
 def _variants_c2(world: int):
     """(name, schedule, workers, grad_reset, torch optimizer, bucket, CUDA graph, channels-last)"""
     K = 1 << 18
+    LB = "fwd+bwd only (no update: lower bound)"
     v = [("torch.optim.SGD(foreach)", "baseline", None, None, "foreach", None, False, False),
+         (LB, "baseline", None, None, "none", None, False, False),
+         ("graph:" + LB, "baseline", None, None, "none", None, True, False),
+         ("cl:graph:" + LB, "baseline", None, None, "none", None, True, True),
          ("torch.optim.SGD(fused)", "baseline", None, None, "fused", None, False, False),
          ("ours:baseline", "baseline", None, None, None, None, False, False),
          ("ours:forward-fusion(per-layer)", "forward-fusion", None, None, None, 0, False, False),
@@ -429,21 +487,35 @@ KEY_ROWS = ("torch.optim.SGD(foreach)", "ours:backward-fusion(w=2,bucket=256K)",
             "graph:ours:backward-fusion(w=2,bucket=256K)", "cl:graph:torch.optim.SGD(foreach)",
             "cl:graph:ours:backward-fusion(w=2,bucket=256K)", "cl:graph:ours:forward-fusion(bucket=256K)")
 SWEEP_ROWS = ("torch.optim.SGD(foreach)", "ours:forward-fusion(bucket=256K)",
+              "graph:fwd+bwd only (no update: lower bound)",
               "ours:backward-fusion(w=2,bucket=256K)", "graph:torch.optim.SGD(foreach)",
               "graph:ours:backward-fusion(w=2,bucket=256K)", "graph:ours:forward-fusion(bucket=256K)")
 
 
 def _speedups(row: dict) -> None:
     """Speed-ups against the matching unfused torch baseline (same graph /
-    layout mode)."""
+    layout mode), and the share of the unfused update phase each schedule
+    hides when a forward+backward-only row (the lower bound) is present."""
+    def torch_row(prefix):
+        for opt in ("SGD", "Adam", "AdamW"):
+            r = row.get(f"{prefix}torch.optim.{opt}(foreach)")
+            if r:
+                return r
+        return None
+    eager = torch_row("")
     for k, v in row.items():
-        mode = k.rsplit("ours:", 1)[0] if "ours:" in k else k.rsplit("torch.optim", 1)[0]
-        base = row.get(mode + "torch.optim.SGD(foreach)") or row.get(mode + "torch.optim.Adam(foreach)")
+        mode = k.rsplit("ours:", 1)[0] if "ours:" in k else k.split("torch.optim", 1)[0] \
+            if "torch.optim" in k else k.split("fwd+bwd", 1)[0]
+        base = torch_row(mode)
         if base:
             v["speedup_vs_unfused_same_mode"] = round(base["ms_per_step"] / v["ms_per_step"], 4)
-        eager = row.get("torch.optim.SGD(foreach)") or row.get("torch.optim.Adam(foreach)")
         if eager:
             v["speedup_vs_eager_torch_foreach"] = round(eager["ms_per_step"] / v["ms_per_step"], 4)
+        lb = row.get(mode + "fwd+bwd only (no update: lower bound)")
+        if base and lb and k.startswith(mode + "ours:"):
+            phase = base["ms_per_step"] - lb["ms_per_step"]
+            if phase > 0:
+                v["unfused_update_phase_hidden"] = round((base["ms_per_step"] - v["ms_per_step"]) / phase, 3)
 
 
 def run_ours(args) -> dict:
@@ -515,15 +587,28 @@ def run_ours(args) -> dict:
             _speedups(row)
             sched[str(b)] = row
         res["schedules"] = sched
-        base_ms = sched[str(args.batch)]["torch.optim.SGD(foreach)"]["ms_per_step"]
-        res["speedup_vs_unfused_torch"] = round(base_ms / ms, 4)
-        res["c3_vgg16_adam"] = run_c3(args, device, dist, flush)
+        row = sched[str(args.batch)]
+        mode = ("cl:" if args.channels_last else "") + ("graph:" if args.graphs else "")
+        same = row.get(mode + "torch.optim.SGD(foreach)") or row["torch.optim.SGD(foreach)"]
+        lb = row.get(mode + "fwd+bwd only (no update: lower bound)")
+        res["vs_unfused_torch"] = {
+            "mode": mode or "eager", "torch_foreach_ms": same["ms_per_step"],
+            "speedup": round(same["ms_per_step"] / ms, 4),
+            "fwd_bwd_only_ms": lb["ms_per_step"] if lb else None,
+            "speedup_vs_eager_torch_foreach": round(row["torch.optim.SGD(foreach)"]["ms_per_step"] / ms, 4)}
+        for wl, key in (("c1", "c1_resnet18_sgdm"), ("c3", "c3_vgg16_adam"),
+                        ("c4", "c4_resnet50_bf16_adamw"), ("c5", "c5_bert_base_adamw")):
+            if wl in args.extras.split(","):
+                res[key] = run_extra(args, wl, device, dist, flush)
         res["e2e"] = e2e(args, device, dist)
         ins = measure_in_situ(args, device, peaks, 5)
         std = measure_update_kernel(args, device, peaks)
+        tr = ncu_traffic("c2_backward_fusion_buckets")
         res["roofline"] = {"bound": "hbm", "kernel": "mt_step_kernel (backward-fusion, side stream)",
                            "achieved": round(ins["achieved_gbs"], 1), "peak": peaks["hbm_gbs"],
-                           "unit": "GB/s", "frac": round(ins["frac"], 4), "traffic": None,
+                           "unit": "GB/s", "frac": round(ins["frac"], 4),
+                           "traffic": (tr or {}).get("dram_bytes_per_launch"),
+                           "traffic_source": (tr or {}).get("source"),
                            "peak_source": peaks["source"],
                            "per_launch": {"avg_bytes": round(ins["avg_bytes"]), "avg_us": round(ins["avg_us"], 3),
                                           "launches_per_step": ins["launches_per_step"]},
@@ -535,27 +620,44 @@ def run_ours(args) -> dict:
     return res
 
 
-def run_c3(args, device, dist, flush) -> dict:
-    """C3 (BASELINE.json configs[2]): VGG-16, 3x224x224, batch 32 per GPU, Adam with
-    coupled weight decay 1e-4 (the paper's setting) -- the update-bound case."""
+def _variants_extra(wl: str):
+    """(name, schedule, workers, torch optimizer, bucket) for the eager extras."""
+    opt = WORKLOADS[wl]["torch"][0]
+    v = [(f"torch.optim.{opt}(foreach)", "baseline", None, "foreach", 0),
+         (f"torch.optim.{opt}(fused)", "baseline", None, "fused", 0),
+         ("fwd+bwd only (no update: lower bound)", "baseline", None, "none", 0),
+         ("ours:baseline", "baseline", None, None, 0),
+         ("ours:forward-fusion(per-layer)", "forward-fusion", None, None, 0),
+         ("ours:backward-fusion(w=2,per-layer)", "backward-fusion", 2, None, 0)]
+    if wl == "c3":
+        v.append(("ours:backward-fusion(w=2,per-layer,capped)", "backward-fusion", -1, None, 0))
+    else:
+        v.append(("ours:forward-fusion(bucket=1M)", "forward-fusion", None, None, 1 << 20))
+        v.append(("ours:backward-fusion(w=2,bucket=1M)", "backward-fusion", 2, None, 1 << 20))
+    return v
+
+
+def run_extra(args, wl: str, device, dist, flush) -> dict:
+    """One of BASELINE.json's other configs on this GPU, eager (Adam/AdamW
+    bias corrections depend on the step index, so those iterations are not
+    replayed from CUDA graphs): C1 ResNet-18/CIFAR SGD-momentum, C3 VGG-16
+    Adam (the update-bound case), C4 ResNet-50 bf16 + fp32 masters AdamW,
+    C5 BERT-base AdamW."""
     import torch
-    b = WORKLOADS["c3"]["batch"]
+    b = WORKLOADS[wl]["batch"]
     steps, warm = max(args.steps // 3, 5), 3
     row = {}
-    for name, sch, w, opt in (("torch.optim.Adam(foreach)", "baseline", None, "foreach"),
-                              ("torch.optim.Adam(fused)", "baseline", None, "fused"),
-                              ("ours:baseline", "baseline", None, None),
-                              ("ours:forward-fusion(per-layer)", "forward-fusion", None, None),
-                              ("ours:backward-fusion(w=2,per-layer)", "backward-fusion", 2, None),
-                              ("ours:backward-fusion(w=2,per-layer,capped)", "backward-fusion", -1, None)):
-        st, *_ = make_runner(args, b, sch, device, workers=w, opt_impl=opt, bucket_elems=0,
-                             graphed=False, workload="c3", channels_last=False)
+    for name, sch, w, opt, be in _variants_extra(wl):
+        st, *_ = make_runner(args, b, sch, device, workers=w, opt_impl=opt, bucket_elems=be,
+                             graphed=False, workload=wl, channels_last=wl in ("c4",))
         t = timed(st, steps, warm, dist, flush)
         row[name] = {"ms_per_step": round(t, 3), "images_per_s": round(dist.world * b * 1e3 / t, 1)}
         del st
         torch.cuda.empty_cache()
     _speedups(row)
-    return {"batch_per_gpu": b, "steps": steps, "warmup": warm, "eager": True, "schedules": row}
+    lb = row.pop("fwd+bwd only (no update: lower bound)")
+    return {"workload": WORKLOADS[wl]["desc"], "batch_per_gpu": b, "steps": steps, "warmup": warm,
+            "eager": True, "fwd_bwd_only_ms": lb["ms_per_step"], "schedules": row}
 
 
 def e2e(args, device, dist) -> dict:

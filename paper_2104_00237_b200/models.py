@@ -208,22 +208,70 @@ CLASSIFIERS = {
 }
 
 
+class BertPretraining(nn.Module):
+    """BERT-base pre-training model (C5): ``transformers.BertForPreTraining``
+    with the default BertConfig (12 layers, hidden 768, vocab 30522), random
+    init, returning both heads' logits.  The MLM decoder weight is tied to the
+    word embeddings (and the decoder bias to the head bias): one Parameter
+    bound to two layers, the reference's shared-parameter case."""
+
+    def __init__(self, **config):
+        super().__init__()
+        from transformers import BertConfig, BertForPreTraining
+        self.net = BertForPreTraining(BertConfig(**config))
+
+    def forward(self, ids):
+        out = self.net(input_ids=ids, return_dict=True)
+        return out.prediction_logits, out.seq_relationship_logits
+
+
+def bert_pretraining_loss(out, target):
+    """Masked-LM cross entropy (label -100 = not masked) + next-sentence CE."""
+    mlm, nsp = out
+    labels, nsp_labels = target
+    return (F.cross_entropy(mlm.reshape(-1, mlm.shape[-1]).float(), labels.reshape(-1),
+                            ignore_index=-100)
+            + F.cross_entropy(nsp.float(), nsp_labels))
+
+
+BERT_SEQ = 128
+BERT_VOCAB = 30522
+
+# non-classifier networks: name -> (constructor, loss)
+NETWORKS = {"bert_base": (BertPretraining, bert_pretraining_loss)}
+
+
 def build_classifier(name: str, device="cuda", dtype=torch.float32, seed: int = 0,
                      channels_last: bool = False, **graph_kw) -> Graph:
-    """A randomly initialised benchmark CNN as a Graph with a cross-entropy loss."""
-    if name not in CLASSIFIERS:
-        raise ConfigError(f"unknown classifier {name!r}, expected one of {sorted(CLASSIFIERS)}")
+    """A randomly initialised benchmark network as a Graph: the CNNs with a
+    cross-entropy loss, ``bert_base`` with the pre-training loss."""
+    if name not in CLASSIFIERS and name not in NETWORKS:
+        raise ConfigError(f"unknown network {name!r}, expected one of "
+                          f"{sorted(CLASSIFIERS) + sorted(NETWORKS)}")
     torch.manual_seed(seed)
+    if name in NETWORKS:
+        ctor, loss = NETWORKS[name]
+        cfg = graph_kw.pop("config", None) or {}
+        return Graph(ctor(**cfg).to(device=device, dtype=dtype), loss, model=name, **graph_kw)
     net = CLASSIFIERS[name][0]().to(device=device, dtype=dtype)
     if channels_last:
         net = net.to(memory_format=torch.channels_last)
     return Graph(net, F.cross_entropy, model=name, **graph_kw)
 
 
-def synthetic_batch(name: str, batch: int, device="cuda", dtype=torch.float32, seed: int = 0):
-    """x ~ N(0, 1), y ~ U{0..classes-1}."""
-    _, shape, classes = CLASSIFIERS[name]
+def synthetic_batch(name: str, batch: int, device="cuda", dtype=torch.float32, seed: int = 0,
+                    seq: int = BERT_SEQ, vocab: int = BERT_VOCAB):
+    """CNNs: x ~ N(0, 1), y ~ U{0..classes-1}.
+    bert_base: ids ~ U{0..30521} [b, 128], 15% of positions carry an MLM label
+    (the original id), the rest -100; next-sentence labels ~ U{0, 1}."""
     g = torch.Generator(device="cpu").manual_seed(seed)
+    if name == "bert_base":
+        ids = torch.randint(0, vocab, (batch, seq), generator=g)
+        masked = torch.rand((batch, seq), generator=g) < 0.15
+        labels = torch.where(masked, ids, torch.full_like(ids, -100))
+        nsp = torch.randint(0, 2, (batch,), generator=g)
+        return ids.to(device), (labels.to(device), nsp.to(device))
+    _, shape, classes = CLASSIFIERS[name]
     x = torch.randn((batch,) + shape, generator=g).to(device=device, dtype=dtype)
     y = torch.randint(0, classes, (batch,), generator=g).to(device)
     return x, y

@@ -158,6 +158,26 @@ def test_classifier_discovery():
     assert sum(p.value.numel() for p in g.parameters) == 11_173_962
 
 
+def test_bert_base_discovery_and_loss():
+    """C5's network: BERT-base pre-training, 206 tensors / 110.1 M parameters
+    (SURVEY.md §8(a)2), the MLM decoder tied to the word embeddings."""
+    g = of.build_classifier("bert_base", device="cpu")
+    assert len(g.parameters) == 206
+    assert sum(p.value.numel() for p in g.parameters) == 110_106_428
+    emb = g.module.net.bert.embeddings.word_embeddings.weight
+    p = g.parameter_of(emb)
+    assert len(p.layers) == 2   # embedding lookup + MLM decoder
+    small = of.build_classifier("bert_base", device="cpu",
+                                config=dict(num_hidden_layers=1, hidden_size=32,
+                                            num_attention_heads=2, intermediate_size=64,
+                                            vocab_size=100))
+    ids, (labels, nsp) = of.models.synthetic_batch("bert_base", 3, device="cpu", seq=16, vocab=100)
+    assert ids.shape == labels.shape == (3, 16) and nsp.shape == (3,)
+    assert ((labels == -100) | (labels == ids)).all()
+    loss = small.forward((ids, (labels, nsp)))
+    assert loss.dim() == 0 and torch.isfinite(loss)
+
+
 def test_tied_parameters_are_one_parameter():
     emb = torch.nn.Embedding(10, 4)
     head = torch.nn.Linear(4, 10, bias=False)

@@ -1,17 +1,24 @@
-# GPU round trip: tests, bench, ncu launch list + full captures of the update kernel
+# GPU round trip: smoke, tests, bench, ncu launch list + full captures of the update kernel
 mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv,noheader
 if [ -z "${SKIP_TESTS}" ]; then
-timeout 900 python -m pytest tests -q -m gpu --durations=10 --timeout 300 -x > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
-grep -E "passed|failed" gpurun_out/pytest_gpu.log
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?
+tail -1 gpurun_out/smoke.log
+timeout 1200 python -m pytest tests -q -m gpu --durations=15 --timeout 400 -x > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
+grep -E "passed|failed|Error" gpurun_out/pytest_gpu.log | tail -5
 fi
-timeout 900 python bench.py ${BENCH_ARGS} > gpurun_out/bench.log 2>&1; echo bench=$?
-tail -c 600 gpurun_out/bench.log
+if [ -z "${SKIP_BENCH}" ]; then
+timeout 1500 python bench.py ${BENCH_ARGS} > gpurun_out/bench.log 2>&1; echo bench=$?
+tail -c 400 gpurun_out/bench.log
+fi
 if [ -n "${NCU}" ]; then
-  # launch list of the headline command (skip the first 3000 launches: build, cudnn autotune, capture)
+  # launch list of the headline command (NVTX-selected timed region)
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "timed/" -c 3000 --csv \
     --log-file gpurun_out/launches.csv python bench.py --no-extras --steps 4 --warmup 3 --instances 1 > gpurun_out/ncu_bench.log 2>&1; echo ncu_list=$?
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:mt_step -s 40 -c 3 \
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:mt_step -s 40 -c 8 \
     -o gpurun_out/prof_bf -f python tools/profile_kernels.py bf > gpurun_out/ncu_bf.log 2>&1; echo ncu_bf=$?
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:mt_step -s 1 -c 1 \
     -o gpurun_out/prof_vgg -f python tools/profile_kernels.py vgg > gpurun_out/ncu_vgg.log 2>&1; echo ncu_vgg=$?
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:mt_step -s 1 -c 1 \
+    -o gpurun_out/prof_bert -f python tools/profile_kernels.py bert > gpurun_out/ncu_bert.log 2>&1; echo ncu_bert=$?
 fi

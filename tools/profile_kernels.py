@@ -2,6 +2,7 @@
 
     python tools/profile_kernels.py bf      # MobileNetV2 b128 backward fusion, bucketed launches
     python tools/profile_kernels.py vgg     # one multi-tensor Adam launch over VGG-16 (138 M params)
+    python tools/profile_kernels.py bert    # one AdamW launch over BERT-base (206 tensors, 110 M)
 """
 
 import sys
@@ -26,9 +27,9 @@ def bf(iters=6):
     torch.cuda.synchronize()
 
 
-def vgg(iters=3):
-    g = of.build_classifier("vgg16", device="cuda")
-    pol = of.OptimizerPolicy("adam", eta=1e-4, grad_reset="none")
+def vgg(iters=3, model="vgg16", kind="adam"):
+    g = of.build_classifier(model, device="cuda")
+    pol = of.OptimizerPolicy(kind, eta=1e-4, grad_reset="none")
     for p in g.parameters:
         p.value.grad = torch.randn_like(p.value) * 0.01
     for _ in range(iters):
@@ -40,5 +41,9 @@ def vgg(iters=3):
     torch.cuda.synchronize()
 
 
+def bert(iters=3):
+    vgg(iters, "bert_base", "adamw")
+
+
 if __name__ == "__main__":
-    {"bf": bf, "vgg": vgg}[sys.argv[1]]()
+    {"bf": bf, "vgg": vgg, "bert": bert}[sys.argv[1]]()

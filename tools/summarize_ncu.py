@@ -63,8 +63,37 @@ def report(path, title):
         print()
 
 
+def traffic(path, key, out_json):
+    """Average DRAM bytes (read + write) and duration per captured launch,
+    merged into ``out_json`` under ``key`` (read by bench.py's roofline)."""
+    import json
+    import os
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True, check=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+
+    def val(r, m):
+        v = float(r[hdr.index(m)].replace(",", ""))
+        u = units[hdr.index(m)]
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-3, "us": 1,
+                 "usecond": 1, "msecond": 1e3, "nsecond": 1e-3}.get(u, 1)
+        return v * scale
+    recs = [(val(r, "dram__bytes_read.sum") + val(r, "dram__bytes_write.sum"),
+             val(r, "gpu__time_duration.sum")) for r in rows[2:]]
+    d = json.load(open(out_json)) if os.path.exists(out_json) else {}
+    d[key] = {"launches": len(recs), "dram_bytes_per_launch": round(sum(b for b, _ in recs) / len(recs)),
+              "gpu_time_us_per_launch": round(sum(t for _, t in recs) / len(recs), 3),
+              "source": f"ncu --set full --clock-control none ({os.path.basename(path)})"}
+    with open(out_json, "w") as fh:
+        json.dump(d, fh, indent=1)
+    print(json.dumps(d[key]))
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "launches":
         launches(sys.argv[2])
+    elif sys.argv[1] == "traffic":
+        traffic(sys.argv[2], sys.argv[3], sys.argv[4])
     else:
         report(sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else sys.argv[2])
