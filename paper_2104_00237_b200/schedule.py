@@ -29,6 +29,7 @@ from __future__ import annotations
 
 import torch
 
+from . import checkpoint
 from . import trace as tr
 from .errors import ConfigError, GlobalInfoRequired
 from .graph import Graph, Parameter
@@ -205,6 +206,7 @@ def run_baseline(graph: Graph, policy: OptimizerPolicy, inp, *, timing: bool = T
                  trace: bool = False) -> StepReport:
     """Three contiguous phases; the update phase is one multi-tensor launch."""
     _reject_newton(policy)
+    checkpoint.attach(graph, policy)
     _leave_forward_fusion(graph, policy)
     policy.begin_iteration()
     tc = tr.ScheduleTrace(BASELINE) if trace else None
@@ -276,6 +278,7 @@ def run_forward_fusion(graph: Graph, policy: OptimizerPolicy, inp, *, timing: bo
     leaders carry a pre-hook.
     """
     _reject_newton(policy)
+    checkpoint.attach(graph, policy)
     if bucket_elems < 0:
         raise ConfigError(f"bucket_elems must be >= 0, got {bucket_elems}")
     eng = _engine(graph, policy, False)
@@ -408,6 +411,7 @@ def run_backward_fusion(graph: Graph, policy: OptimizerPolicy, inp, workers: int
             f"backward-fusion cannot host {policy.kind!r}"
             + (" with global-norm clipping" if policy.clip_norm is not None else ""))
     _reject_newton(policy)
+    checkpoint.attach(graph, policy)
     if workers < 1:
         raise ConfigError(f"workers must be >= 1, got {workers}")
     if bucket_elems < 0:

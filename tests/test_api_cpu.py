@@ -199,3 +199,15 @@ def test_missing_library_fails_loudly(monkeypatch, tmp_path):
     monkeypatch.setenv("OPTFUSE_B200_LIB", str(tmp_path / "nope.so"))
     with pytest.raises(errors.NativeLibraryError, match="no CPU fallback"):
         _native.lib()
+
+
+def test_checkpoint_rejects_foreign_or_mismatched_state():
+    from paper_2104_00237_b200 import checkpoint
+    g = of.build_model("chain", layers=2, width=3, device="cpu")
+    pol = of.OptimizerPolicy("adam")
+    with pytest.raises(errors.ConfigError):
+        checkpoint.load_state_dict(g, pol, {"format": "something-else"})
+    sd = {"format": "optfuse-b200/1", "policy": {"kind": "sgd"}, "model": {}, "history": {},
+          "master": {}}
+    with pytest.raises(errors.ConfigError, match="checkpoint is for"):
+        checkpoint.load_state_dict(g, pol, sd)
