@@ -316,9 +316,11 @@ def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
             x = x.to(torch.bfloat16) if x.is_floating_point() else x
         pol = of.OptimizerPolicy(wl["kind"], **wl["hp"], grad_reset=grad_reset or args.grad_reset)
         w = args.workers if workers is None else workers
-        ctas = None
+        ctas, prio = None, "high"
         if w == -1:       # side stream with the update grid capped to a third of the SMs
             w, ctas = 2, max(8, torch.cuda.get_device_properties(device).multi_processor_count // 3)
+        elif w == -2:     # side stream at the compute stream's (default) priority
+            w, prio = 2, "low"
         if schedule == "baseline":
             def run(inp):
                 return of.run_baseline(g, pol, inp, timing=False).loss
@@ -332,11 +334,13 @@ def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
 
             def run(inp):
                 return of.run_backward_fusion(g, pol, inp, workers=w, timing=False,
-                                              bucket_elems=be, update_ctas=ctas).loss
+                                              bucket_elems=be, update_ctas=ctas,
+                                              update_priority=prio).loss
         owner = g
     if graphed:
-        cap = CapturedStep(run, (x, y), warmup=3,
-                           policy=pol if isinstance(pol, of.OptimizerPolicy) else None)
+        ours = isinstance(pol, of.OptimizerPolicy)
+        cap = CapturedStep(run, (x, y), warmup=3, policy=pol if ours else None,
+                           graph=owner if ours else None)
         return cap, owner, pol
 
     def step():
@@ -422,6 +426,9 @@ def measure_in_situ(args, device, peaks, reps: int = 5) -> dict:
     native = eng.native
     # element count of every group, from one profiled pass
     step()
+    for p in g.parameters:
+        if p.value.grad is None:
+            p.value.grad = torch.randn_like(p.value) * 0.01
     native.set_profile(True)
     for gi in range(native.num_groups):
         native.launch_group(gi, sync=False)
@@ -432,6 +439,13 @@ def measure_in_situ(args, device, peaks, reps: int = 5) -> dict:
     ms = []
     for _ in range(reps):
         step()
+        # the step released its gradients (grad_reset="none"): give every
+        # parameter one again outside the timed sequence, so the replayed
+        # launches allocate nothing
+        for p in g.parameters:
+            if p.value.grad is None:
+                p.value.grad = torch.randn_like(p.value) * 0.01
+        torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(eng.stream):
             torch.cuda._sleep(20_000_000)
@@ -645,55 +659,78 @@ OWN_LB = "fwd+bwd only (bf16 module as ours: lower bound for ours)"
 
 
 def _variants_extra(wl: str):
-    """(name, schedule, workers, torch optimizer, bucket) for the eager extras."""
+    """(name, schedule, workers, torch optimizer, bucket, CUDA graph) for the extras."""
     opt = WORKLOADS[wl]["torch"][0]
-    v = [(f"torch.optim.{opt}(foreach)", "baseline", None, "foreach", 0),
-         (f"torch.optim.{opt}(fused)", "baseline", None, "fused", 0),
-         ("fwd+bwd only (no update: lower bound)", "baseline", None, "none", 0),
-         ("ours:baseline", "baseline", None, None, 0),
-         ("ours:forward-fusion(per-layer)", "forward-fusion", None, None, 0),
-         ("ours:backward-fusion(w=2,per-layer)", "backward-fusion", 2, None, 0)]
+    LB = "fwd+bwd only (no update: lower bound)"
+    v = [(f"torch.optim.{opt}(foreach)", "baseline", None, "foreach", 0, False),
+         (f"torch.optim.{opt}(fused)", "baseline", None, "fused", 0, False),
+         (LB, "baseline", None, "none", 0, False),
+         ("ours:baseline", "baseline", None, None, 0, False),
+         ("ours:forward-fusion(per-layer)", "forward-fusion", None, None, 0, False),
+         ("ours:backward-fusion(w=2,per-layer)", "backward-fusion", 2, None, 0, False),
+         ("ours:backward-fusion(w=2,per-layer,default-prio)", "backward-fusion", -2, None, 0, False)]
     if WORKLOADS[wl].get("mixed"):
-        v.append((OWN_LB, "baseline", None, "none-mixed", 0))
+        v.append((OWN_LB, "baseline", None, "none-mixed", 0, False))
     if wl == "c3":
-        v.append(("ours:backward-fusion(w=2,per-layer,capped)", "backward-fusion", -1, None, 0))
+        v.append(("ours:backward-fusion(w=2,per-layer,capped)", "backward-fusion", -1, None, 0, False))
     else:
-        v.append(("ours:forward-fusion(bucket=1M)", "forward-fusion", None, None, 1 << 20))
-        v.append(("ours:backward-fusion(w=2,bucket=1M)", "backward-fusion", 2, None, 1 << 20))
+        v.append(("ours:forward-fusion(bucket=1M)", "forward-fusion", None, None, 1 << 20, False))
+        v.append(("ours:backward-fusion(w=2,bucket=1M)", "backward-fusion", 2, None, 1 << 20, False))
+    # the same iteration captured as one CUDA graph (Adam/AdamW replay through
+    # the device-side step index; torch's Adam with capturable=True)
+    v += [(f"graph:torch.optim.{opt}(foreach)", "baseline", None, "foreach", 0, True),
+          (f"graph:torch.optim.{opt}(fused)", "baseline", None, "fused", 0, True),
+          ("graph:" + LB, "baseline", None, "none", 0, True),
+          ("graph:ours:baseline", "baseline", None, None, 0, True),
+          ("graph:ours:forward-fusion(bucket=1M)", "forward-fusion", None, None, 1 << 20, True),
+          ("graph:ours:backward-fusion(w=2,bucket=1M)", "backward-fusion", 2, None, 1 << 20, True)]
+    if WORKLOADS[wl].get("mixed"):
+        v.append(("graph:" + OWN_LB, "baseline", None, "none-mixed", 0, True))
     return v
 
 
 def run_extra(args, wl: str, device, dist, flush) -> dict:
-    """One of BASELINE.json's other configs on this GPU, eager (Adam/AdamW
-    bias corrections depend on the step index, so those iterations are not
-    replayed from CUDA graphs): C1 ResNet-18/CIFAR SGD-momentum, C3 VGG-16
-    Adam (the update-bound case), C4 ResNet-50 bf16 + fp32 masters AdamW,
-    C5 BERT-base AdamW."""
+    """One of BASELINE.json's other configs on this GPU, eager and captured as
+    CUDA graphs: C1 ResNet-18/CIFAR SGD-momentum, C3 VGG-16 Adam (the
+    update-bound case), C4 ResNet-50 bf16 + fp32 masters AdamW, C5 BERT-base
+    AdamW."""
     import torch
     b = WORKLOADS[wl]["batch"]
     steps, warm = max(args.steps // 3, 5), 3
-    row = {}
-    for name, sch, w, opt, be in _variants_extra(wl):
-        st, *_ = make_runner(args, b, sch, device, workers=w, opt_impl=opt, bucket_elems=be,
-                             graphed=False, workload=wl, channels_last=wl in ("c4",))
-        t = timed(st, steps, warm, dist, flush)
+    row, failed = {}, {}
+    for name, sch, w, opt, be, gph in _variants_extra(wl):
+        if gph and dist.world > 1:
+            continue
+        try:
+            st, *_ = make_runner(args, b, sch, device, workers=w, opt_impl=opt, bucket_elems=be,
+                                 graphed=gph, workload=wl, channels_last=wl in ("c4",))
+            t = timed(st, steps, warm, dist, flush)
+        except Exception as e:  # noqa: BLE001 -- report, keep the other rows
+            failed[name] = f"{type(e).__name__}: {str(e).splitlines()[0][:160] if str(e) else ''}"
+            torch.cuda.synchronize()
+            continue
         row[name] = {"ms_per_step": round(t, 3), "images_per_s": round(dist.world * b * 1e3 / t, 1)}
         del st
         torch.cuda.empty_cache()
     _speedups(row)
-    lb = row.pop("fwd+bwd only (no update: lower bound)")
-    own = row.pop(OWN_LB, None)
-    out = {"workload": WORKLOADS[wl]["desc"], "batch_per_gpu": b, "steps": steps, "warmup": warm,
-           "eager": True, "fwd_bwd_only_ms": lb["ms_per_step"]}
-    if own is not None:
-        # different model math (bf16 module vs fp32 + autocast): ours is judged
-        # against its own forward+backward floor, not the torch phase
-        out["fwd_bwd_only_ms_ours_math"] = own["ms_per_step"]
-        for k, v in row.items():
-            if k.startswith("ours:"):
-                v.pop("unfused_update_phase_hidden", None)
-                v["over_own_fwd_bwd_ms"] = round(v["ms_per_step"] - own["ms_per_step"], 3)
+    out = {"workload": WORKLOADS[wl]["desc"], "batch_per_gpu": b, "steps": steps, "warmup": warm}
+    for mode in ("", "graph:"):
+        lb = row.pop(mode + "fwd+bwd only (no update: lower bound)", None)
+        own = row.pop(mode + OWN_LB, None)
+        key = mode.rstrip(":") or "eager"
+        if lb is not None:
+            out[f"fwd_bwd_only_ms_{key}"] = lb["ms_per_step"]
+        if own is not None:
+            # different model math (bf16 module vs fp32 + autocast): ours is judged
+            # against its own forward+backward floor, not the torch phase
+            out[f"fwd_bwd_only_ms_ours_math_{key}"] = own["ms_per_step"]
+            for k, v in row.items():
+                if k.startswith(mode + "ours:"):
+                    v.pop("unfused_update_phase_hidden", None)
+                    v["over_own_fwd_bwd_ms"] = round(v["ms_per_step"] - own["ms_per_step"], 3)
     out["schedules"] = row
+    if failed:
+        out["failed"] = failed
     return out
 
 

@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define OF_ABI_VERSION 1
+#define OF_ABI_VERSION 2
 
 typedef enum of_status {
   OF_OK = 0,
@@ -73,6 +73,7 @@ typedef enum of_kind {
 /* step flags */
 #define OF_FLAG_ZERO_GRAD 0x1u   /* write grad = 0 after reading it (optim.py:111) */
 #define OF_FLAG_SHADOW_BF16 0x2u /* also write a bf16 copy of the new parameter */
+#define OF_FLAG_DEVICE_STEP 0x4u /* read the step index on the device (see of_hparams) */
 
 /* Hyper-parameters of one policy step (optim.py:42-51).  Scalars are the
  * Python doubles; the library rounds them to the tensor precision. */
@@ -90,6 +91,16 @@ typedef struct of_hparams {
   double rho;
   double bias_correction1; /* ADAM/ADAMW: 1 - beta1**t, in double (optim.py:145) */
   double bias_correction2; /* ADAM/ADAMW: 1 - beta2**t, in double (optim.py:146) */
+  /* OF_FLAG_DEVICE_STEP (ABI 2): the step-dependent scalars are read on the
+   * device when the kernel runs, so a launch captured into a CUDA graph stays
+   * correct on every replay.  The step index is t = t_base + *step_offset_dev;
+   * row t of step_table_dev (step_table_rows rows of 2 doubles) holds the
+   * host's {1 - beta1**t, 1 - beta2**t}, and bias_correction1/2 are ignored.
+   * Rows outside [1, step_table_rows) are clamped (the host keeps t inside). */
+  const int64_t* step_offset_dev;
+  const double* step_table_dev;
+  int64_t step_table_rows;
+  int64_t t_base;
 } of_hparams;
 
 /* A list of parameters updated by one launch.  Arrays live in HOST memory and
@@ -134,6 +145,11 @@ int of_adam_mt(const of_tensor_list* list, double eta, double beta1, double beta
                double epsilon, double weight_decay, double bias_correction1,
                double bias_correction2, int decoupled_weight_decay,
                const float* grad_scale_dev, uint32_t flags, void* stream);
+
+/* *step_offset_dev += delta on `stream` (one thread): the first node of a
+ * captured iteration, advancing the device step index of OF_FLAG_DEVICE_STEP
+ * launches once per replay. */
+int of_step_advance(int64_t* step_offset_dev, int64_t delta, void* stream);
 
 /* Sum of squares of every grad in `list`, accumulated in f64 with a fixed
  * (deterministic) reduction order (optim.py:160-164).  Uses `workspace_dev`

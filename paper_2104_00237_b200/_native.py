@@ -20,6 +20,8 @@ OF_OK, OF_ERR_INVALID, OF_ERR_UNSUPPORTED, OF_ERR_CUDA = 0, 1, 2, 3
 OF_F32, OF_F64, OF_BF16 = 0, 1, 2
 OF_FLAG_ZERO_GRAD = 0x1
 OF_FLAG_SHADOW_BF16 = 0x2
+OF_FLAG_DEVICE_STEP = 0x4
+ABI_VERSION = 2
 
 # of_kind (optim.py:22 minus newton, plus adamw)
 KIND_CODES = {"sgd": 0, "sgd-momentum": 1, "adagrad": 2, "rmsprop": 3, "adadelta": 4,
@@ -27,8 +29,8 @@ KIND_CODES = {"sgd": 0, "sgd-momentum": 1, "adagrad": 2, "rmsprop": 3, "adadelta
 
 # every symbol include/optfuse_b200.h declares (checked by tests/test_native_abi.py)
 SYMBOLS = ("of_abi_version", "of_status_string", "of_last_error", "of_launch_count",
-           "of_policy_step_mt", "of_sgdm_mt", "of_adam_mt", "of_sqnorm_workspace_len",
-           "of_sqnorm_mt", "of_clip_coef")
+           "of_policy_step_mt", "of_sgdm_mt", "of_adam_mt", "of_step_advance",
+           "of_sqnorm_workspace_len", "of_sqnorm_mt", "of_clip_coef")
 
 _vp = ctypes.c_void_p
 _PP = ctypes.POINTER(ctypes.c_void_p)
@@ -39,7 +41,9 @@ class OfHparams(ctypes.Structure):
                 ("eta", ctypes.c_double), ("alpha", ctypes.c_double),
                 ("weight_decay", ctypes.c_double), ("epsilon", ctypes.c_double),
                 ("beta1", ctypes.c_double), ("beta2", ctypes.c_double), ("rho", ctypes.c_double),
-                ("bias_correction1", ctypes.c_double), ("bias_correction2", ctypes.c_double)]
+                ("bias_correction1", ctypes.c_double), ("bias_correction2", ctypes.c_double),
+                ("step_offset_dev", _vp), ("step_table_dev", _vp),
+                ("step_table_rows", ctypes.c_int64), ("t_base", ctypes.c_int64)]
 
 
 class OfTensorList(ctypes.Structure):
@@ -80,14 +84,17 @@ def lib():
     so.of_adam_mt.restype = ctypes.c_int
     so.of_adam_mt.argtypes = [ctypes.POINTER(OfTensorList)] + [ctypes.c_double] * 7 + [
         ctypes.c_int, _vp, ctypes.c_uint32, _vp]
+    so.of_step_advance.restype = ctypes.c_int
+    so.of_step_advance.argtypes = [_vp, ctypes.c_int64, _vp]
     so.of_sqnorm_workspace_len.restype = ctypes.c_int64
     so.of_sqnorm_mt.restype = ctypes.c_int
     so.of_sqnorm_mt.argtypes = [ctypes.POINTER(OfTensorList), _vp, ctypes.c_int64, _vp,
                                 ctypes.c_int, _vp]
     so.of_clip_coef.restype = ctypes.c_int
     so.of_clip_coef.argtypes = [_vp, ctypes.c_double, _vp, _vp, _vp]
-    if so.of_abi_version() != 1:
-        raise NativeLibraryError(f"{path}: ABI version {so.of_abi_version()} != 1")
+    if so.of_abi_version() != ABI_VERSION:
+        raise NativeLibraryError(f"{path}: ABI version {so.of_abi_version()} != {ABI_VERSION} "
+                                 "(stale build: rerun __graft_entry__.build())")
     _lib = so
     return so
 

@@ -142,7 +142,9 @@ class Engine : public std::enable_shared_from_this<Engine> {
 
   void set_hparams(int kind, double eta, double alpha, double wd, double eps, double b1, double b2,
                    double rho, double bc1, double bc2, int64_t flags, bool release_grads,
-                   c10::optional<at::Tensor> grad_scale, int max_ctas) {
+                   c10::optional<at::Tensor> grad_scale, int max_ctas,
+                   c10::optional<at::Tensor> step_offset, c10::optional<at::Tensor> step_table,
+                   int64_t t_base) {
     hp_.kind = kind;
     hp_.max_ctas = max_ctas;
     hp_.eta = eta;
@@ -157,6 +159,13 @@ class Engine : public std::enable_shared_from_this<Engine> {
     flags_ = static_cast<uint32_t>(flags);
     release_ = release_grads;
     gscale_ = grad_scale.has_value() ? *grad_scale : at::Tensor();
+    // OF_FLAG_DEVICE_STEP: step index read on the device (CUDA-graph replay)
+    step_offset_ = step_offset.has_value() ? *step_offset : at::Tensor();
+    step_table_ = step_table.has_value() ? *step_table : at::Tensor();
+    hp_.step_offset_dev = step_offset_.defined() ? step_offset_.data_ptr<int64_t>() : nullptr;
+    hp_.step_table_dev = step_table_.defined() ? step_table_.data_ptr<double>() : nullptr;
+    hp_.step_table_rows = step_table_.defined() ? step_table_.size(0) : 0;
+    hp_.t_base = t_base;
   }
 
   // (Re)installs this engine's hook on every grouped parameter, replacing
@@ -412,7 +421,7 @@ class Engine : public std::enable_shared_from_this<Engine> {
   of_hparams hp_;
   uint32_t flags_ = 0;
   bool release_ = false;
-  at::Tensor gscale_;
+  at::Tensor gscale_, step_offset_, step_table_;
   cudaStream_t side_ = nullptr;
   cudaEvent_t join_ = nullptr;
   bool armed_ = false;

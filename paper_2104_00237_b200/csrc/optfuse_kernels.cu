@@ -101,9 +101,19 @@ struct CoupledWd {
   }
 };
 
+// Step-dependent scalars read on the device (OF_FLAG_DEVICE_STEP); only the
+// Adam kinds have any.
+struct StepSrc {
+  const int64_t* offset;   // nullptr: host mode (constants already in the functor)
+  const double* table;     // [rows][2] = {1 - beta1**t, 1 - beta2**t}
+  int64_t rows;
+  int64_t t_base;
+};
+
 template <class T>
 struct SgdOp {  // optim.py:119-120
   static constexpr int kSlots = 0;
+  __device__ __forceinline__ void set_step(double, double) {}  // step-independent
   CoupledWd<T> wd;
   T neg_eta;
   __device__ __forceinline__ void operator()(T& p, T g, T&, T&) const {
@@ -115,6 +125,7 @@ struct SgdOp {  // optim.py:119-120
 template <class T>
 struct SgdMomentumOp {  // optim.py:121-125
   static constexpr int kSlots = 1;
+  __device__ __forceinline__ void set_step(double, double) {}  // step-independent
   CoupledWd<T> wd;
   T neg_eta, alpha;
   __device__ __forceinline__ void operator()(T& p, T g, T& buf, T&) const {
@@ -128,6 +139,7 @@ struct SgdMomentumOp {  // optim.py:121-125
 template <class T>
 struct AdagradOp {  // optim.py:126-129
   static constexpr int kSlots = 1;
+  __device__ __forceinline__ void set_step(double, double) {}  // step-independent
   CoupledWd<T> wd;
   T neg_eta, eps;
   __device__ __forceinline__ void operator()(T& p, T g, T& acc, T&) const {
@@ -140,6 +152,7 @@ struct AdagradOp {  // optim.py:126-129
 template <class T>
 struct RmspropOp {  // optim.py:130-133
   static constexpr int kSlots = 1;
+  __device__ __forceinline__ void set_step(double, double) {}  // step-independent
   CoupledWd<T> wd;
   T neg_eta, eps, rho, one_minus_rho;
   __device__ __forceinline__ void operator()(T& p, T g, T& sq, T&) const {
@@ -152,6 +165,7 @@ struct RmspropOp {  // optim.py:130-133
 template <class T>
 struct AdadeltaOp {  // optim.py:134-140
   static constexpr int kSlots = 2;
+  __device__ __forceinline__ void set_step(double, double) {}  // step-independent
   CoupledWd<T> wd;
   T neg_eta, eps, rho, one_minus_rho;
   __device__ __forceinline__ void operator()(T& p, T g, T& sq, T& acc) const {
@@ -176,6 +190,8 @@ struct AdamOp {  // optim.py:141-148
     const T v_hat = o_div(v, bc2);
     p = o_add(p, o_div(o_mul(neg_eta, m_hat), o_add(o_sqrt(v_hat), eps)));
   }
+  // the host rounds the same doubles once (static_cast<T>)
+  __device__ __forceinline__ void set_step(double c1, double c2) { bc1 = T(c1); bc2 = T(c2); }
 };
 
 // AdamW is not in the reference (SPEC.md:244 puts decoupled decay out of
@@ -188,6 +204,13 @@ struct AdamWOp {
   static constexpr int kSlots = 2;
   T decay, w1, beta2, one_minus_beta2, bc2_sqrt, eps, neg_step;
   bool decay_on, w1_small;
+  double eta;
+  // same double expressions as the host side (sqrt and division are
+  // correctly rounded on both), then one rounding to T
+  __device__ __forceinline__ void set_step(double c1, double c2) {
+    bc2_sqrt = T(__dsqrt_rn(c2));
+    neg_step = T(-__ddiv_rn(eta, c1));
+  }
   __device__ __forceinline__ void operator()(T& p, T g, T& m, T& v) const {
     if (decay_on) p = o_mul(p, decay);
     const T diff = o_sub(g, m);
@@ -287,9 +310,15 @@ __device__ __forceinline__ bool aligned(const void* p, unsigned a) {
 // use UNR=1 so that even a few MB spread over more CTAs than there are SMs.
 template <class Op, class T, class G, int CAP, int UNR>
 __global__ void __launch_bounds__(kThreads)
-mt_step_kernel(const __grid_constant__ MTParams<CAP> mp, const Op op,
-               const float* __restrict__ gscale, uint32_t flags) {
+mt_step_kernel(const __grid_constant__ MTParams<CAP> mp, const Op op_in,
+               const float* __restrict__ gscale, uint32_t flags, const StepSrc step) {
   using GV = typename GradVal<G>::type;
+  Op op = op_in;
+  if (step.offset != nullptr) {  // OF_FLAG_DEVICE_STEP: this replay's step index
+    int64_t t = step.t_base + *step.offset;
+    t = t < 1 ? 1 : (t >= step.rows ? step.rows - 1 : t);
+    op.set_step(step.table[2 * t], step.table[2 * t + 1]);
+  }
   constexpr int kTileU = kThreads * kVec * UNR;
   constexpr int kRoundMax = sizeof(T) == 8 ? 2 : 4;
   constexpr int kRound = UNR < kRoundMax ? UNR : kRoundMax;  // vectors in flight per thread
@@ -421,6 +450,8 @@ __global__ void clip_coef_kernel(const double* sq, double max_norm, float* coef,
   if (factor_out) *factor_out = factor;
 }
 
+__global__ void step_advance_kernel(int64_t* offset, int64_t delta) { *offset += delta; }
+
 // ---------------------------------------------------------------------------
 // Host side: validation, packing, dispatch.
 // ---------------------------------------------------------------------------
@@ -483,7 +514,8 @@ int64_t pack(const of_tensor_list* l, int first, int count, MTParams<CAP>& mp, i
 
 template <class Op, class T, class G, int CAP>
 int launch_step_chunk(const of_tensor_list* l, int first, int count, const Op& op,
-                      const float* gscale, uint32_t flags, int max_ctas, cudaStream_t s) {
+                      const float* gscale, uint32_t flags, const StepSrc& step, int max_ctas,
+                      cudaStream_t s) {
   MTParams<CAP> mp;
   int64_t tiles = pack<CAP>(l, first, count, mp, kTile);
   if (tiles == 0) return OF_OK;
@@ -493,36 +525,36 @@ int launch_step_chunk(const of_tensor_list* l, int first, int count, const Op& o
     // small launch: 1024-element tiles, 4x the CTAs for the same bytes
     tiles = pack<CAP>(l, first, count, mp, kThreads * kVec);
     const int grid = static_cast<int>(tiles < cap ? tiles : cap);
-    mt_step_kernel<Op, T, G, CAP, 1><<<grid, kThreads, 0, s>>>(mp, op, gscale, flags);
+    mt_step_kernel<Op, T, G, CAP, 1><<<grid, kThreads, 0, s>>>(mp, op, gscale, flags, step);
     return check_launch("mt_step_kernel");
   }
   if (tiles > INT32_MAX) return fail(OF_ERR_INVALID, "tensor list too large for one launch");
   const int grid = static_cast<int>(tiles < cap ? tiles : cap);
-  mt_step_kernel<Op, T, G, CAP, kUnroll><<<grid, kThreads, 0, s>>>(mp, op, gscale, flags);
+  mt_step_kernel<Op, T, G, CAP, kUnroll><<<grid, kThreads, 0, s>>>(mp, op, gscale, flags, step);
   return check_launch("mt_step_kernel");
 }
 
 template <class Op, class T, class G>
 int launch_step(const of_tensor_list* l, const Op& op, const float* gscale, uint32_t flags,
-                int max_ctas, cudaStream_t s) {
+                const StepSrc& step, int max_ctas, cudaStream_t s) {
   int first = 0;
   while (first < l->n) {
     const int left = l->n - first;
     int st;
     if (left <= 4) {
-      st = launch_step_chunk<Op, T, G, 4>(l, first, left, op, gscale, flags, max_ctas, s);
+      st = launch_step_chunk<Op, T, G, 4>(l, first, left, op, gscale, flags, step, max_ctas, s);
       first += left;
     } else if (left <= 16) {
-      st = launch_step_chunk<Op, T, G, 16>(l, first, left, op, gscale, flags, max_ctas, s);
+      st = launch_step_chunk<Op, T, G, 16>(l, first, left, op, gscale, flags, step, max_ctas, s);
       first += left;
     } else if (left <= 64) {
-      st = launch_step_chunk<Op, T, G, 64>(l, first, left, op, gscale, flags, max_ctas, s);
+      st = launch_step_chunk<Op, T, G, 64>(l, first, left, op, gscale, flags, step, max_ctas, s);
       first += left;
     } else {
       // up to 256 tensors in one launch: a 13 KB parameter block (CUDA >= 12.1
       // accepts up to 32 KB), so a whole CNN's parameter set is one kernel
       const int c = left < kCapMax ? left : kCapMax;
-      st = launch_step_chunk<Op, T, G, kCapMax>(l, first, c, op, gscale, flags, max_ctas, s);
+      st = launch_step_chunk<Op, T, G, kCapMax>(l, first, c, op, gscale, flags, step, max_ctas, s);
       first += c;
     }
     if (st != OF_OK) return st;
@@ -539,35 +571,39 @@ template <class T, class G>
 int dispatch_kind(const of_tensor_list* l, const of_hparams* hp, const float* gscale,
                   uint32_t flags, cudaStream_t s) {
   const T neg_eta = static_cast<T>(-hp->eta);
+  StepSrc step{nullptr, nullptr, 0, 0};
+  if (flags & OF_FLAG_DEVICE_STEP)
+    step = StepSrc{hp->step_offset_dev, hp->step_table_dev, hp->step_table_rows, hp->t_base};
+  flags &= ~OF_FLAG_DEVICE_STEP;
   switch (hp->kind) {
     case OF_SGD: {
       SgdOp<T> op{coupled<T>(hp), neg_eta};
-      return launch_step<SgdOp<T>, T, G>(l, op, gscale, flags, hp->max_ctas, s);
+      return launch_step<SgdOp<T>, T, G>(l, op, gscale, flags, step, hp->max_ctas, s);
     }
     case OF_SGD_MOMENTUM: {
       SgdMomentumOp<T> op{coupled<T>(hp), neg_eta, static_cast<T>(hp->alpha)};
-      return launch_step<SgdMomentumOp<T>, T, G>(l, op, gscale, flags, hp->max_ctas, s);
+      return launch_step<SgdMomentumOp<T>, T, G>(l, op, gscale, flags, step, hp->max_ctas, s);
     }
     case OF_ADAGRAD: {
       AdagradOp<T> op{coupled<T>(hp), neg_eta, static_cast<T>(hp->epsilon)};
-      return launch_step<AdagradOp<T>, T, G>(l, op, gscale, flags, hp->max_ctas, s);
+      return launch_step<AdagradOp<T>, T, G>(l, op, gscale, flags, step, hp->max_ctas, s);
     }
     case OF_RMSPROP: {
       RmspropOp<T> op{coupled<T>(hp), neg_eta, static_cast<T>(hp->epsilon),
                       static_cast<T>(hp->rho), static_cast<T>(1.0 - hp->rho)};
-      return launch_step<RmspropOp<T>, T, G>(l, op, gscale, flags, hp->max_ctas, s);
+      return launch_step<RmspropOp<T>, T, G>(l, op, gscale, flags, step, hp->max_ctas, s);
     }
     case OF_ADADELTA: {
       AdadeltaOp<T> op{coupled<T>(hp), neg_eta, static_cast<T>(hp->epsilon),
                        static_cast<T>(hp->rho), static_cast<T>(1.0 - hp->rho)};
-      return launch_step<AdadeltaOp<T>, T, G>(l, op, gscale, flags, hp->max_ctas, s);
+      return launch_step<AdadeltaOp<T>, T, G>(l, op, gscale, flags, step, hp->max_ctas, s);
     }
     case OF_ADAM: {
       AdamOp<T> op{coupled<T>(hp), neg_eta, static_cast<T>(hp->epsilon),
                    static_cast<T>(hp->beta1), static_cast<T>(hp->beta2),
                    static_cast<T>(1.0 - hp->beta1), static_cast<T>(1.0 - hp->beta2),
                    static_cast<T>(hp->bias_correction1), static_cast<T>(hp->bias_correction2)};
-      return launch_step<AdamOp<T>, T, G>(l, op, gscale, flags, hp->max_ctas, s);
+      return launch_step<AdamOp<T>, T, G>(l, op, gscale, flags, step, hp->max_ctas, s);
     }
     case OF_ADAMW: {
       const double w1 = 1.0 - hp->beta1;
@@ -575,8 +611,8 @@ int dispatch_kind(const of_tensor_list* l, const of_hparams* hp, const float* gs
                     static_cast<T>(hp->beta2), static_cast<T>(1.0 - hp->beta2),
                     static_cast<T>(std::sqrt(hp->bias_correction2)), static_cast<T>(hp->epsilon),
                     static_cast<T>(-(hp->eta / hp->bias_correction1)),
-                    hp->weight_decay != 0.0, std::fabs(w1) < 0.5};
-      return launch_step<AdamWOp<T>, T, G>(l, op, gscale, flags, hp->max_ctas, s);
+                    hp->weight_decay != 0.0, std::fabs(w1) < 0.5, hp->eta};
+      return launch_step<AdamWOp<T>, T, G>(l, op, gscale, flags, step, hp->max_ctas, s);
     }
     default:
       return fail(OF_ERR_INVALID, "unknown optimizer kind %d", hp->kind);
@@ -649,12 +685,18 @@ int of_policy_step_mt(const of_tensor_list* list, const of_hparams* hp,
   if (!hp) return fail(OF_ERR_INVALID, "hparams is NULL");
   const int slots = slots_of(hp->kind);
   if (slots < 0) return fail(OF_ERR_INVALID, "unknown optimizer kind %d", hp->kind);
-  if (flags & ~(OF_FLAG_ZERO_GRAD | OF_FLAG_SHADOW_BF16))
+  if (flags & ~(OF_FLAG_ZERO_GRAD | OF_FLAG_SHADOW_BF16 | OF_FLAG_DEVICE_STEP))
     return fail(OF_ERR_INVALID, "unknown flags 0x%x", flags);
   if (!(hp->eta > 0.0)) return fail(OF_ERR_INVALID, "step size must be > 0, got %g", hp->eta);
-  if ((hp->kind == OF_ADAM || hp->kind == OF_ADAMW) &&
-      (hp->bias_correction1 == 0.0 || hp->bias_correction2 == 0.0))
+  if (flags & OF_FLAG_DEVICE_STEP) {
+    if (!hp->step_offset_dev || !hp->step_table_dev)
+      return fail(OF_ERR_INVALID, "OF_FLAG_DEVICE_STEP needs step_offset_dev and step_table_dev");
+    if (hp->step_table_rows < 2)
+      return fail(OF_ERR_INVALID, "step table needs >= 2 rows, got %lld", (long long)hp->step_table_rows);
+  } else if ((hp->kind == OF_ADAM || hp->kind == OF_ADAMW) &&
+             (hp->bias_correction1 == 0.0 || hp->bias_correction2 == 0.0)) {
     return fail(OF_ERR_INVALID, "adam bias corrections must be non-zero (step index t >= 1)");
+  }
   int st = validate_list(list, slots, (flags & OF_FLAG_SHADOW_BF16) != 0, false);
   if (st != OF_OK || list->n == 0) return st;
   if (hp->max_ctas < 0) return fail(OF_ERR_INVALID, "max_ctas must be >= 0, got %d", hp->max_ctas);
@@ -690,6 +732,13 @@ int of_adam_mt(const of_tensor_list* list, double eta, double beta1, double beta
   hp.bias_correction1 = bias_correction1;
   hp.bias_correction2 = bias_correction2;
   return of_policy_step_mt(list, &hp, grad_scale_dev, flags, stream);
+}
+
+int of_step_advance(int64_t* step_offset_dev, int64_t delta, void* stream) {
+  g_err[0] = '\0';
+  if (!step_offset_dev) return fail(OF_ERR_INVALID, "step_offset_dev is NULL");
+  step_advance_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(step_offset_dev, delta);
+  return check_launch("step_advance_kernel");
 }
 
 int64_t of_sqnorm_workspace_len(void) { return kSqnormWorkspace; }

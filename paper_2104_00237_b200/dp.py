@@ -7,7 +7,9 @@ so it shards naturally: rank r owns a contiguous 1/W slice of every bucket
 (and only that slice of the optimizer history -- state memory / W).
 
 Layout (per bucket = consecutive layers in backward order, ``launch_groups``):
-  flat_param [padded]  -- the module's parameters become views into it
+  flat_param [padded]  -- the module's parameters become views into it, each
+                          starting on a 128-byte boundary (gaps stay zero:
+                          a zero gradient on a zero parameter updates to zero)
   flat_grad  [padded]  -- ``param.grad`` views; AccumulateGrad adds in place
   grad_shard [S], history shards [S] per slot, S = padded / W (padded to W*4
   elements so every shard starts 16-byte aligned for the vector path)
@@ -37,8 +39,8 @@ DEFAULT_BUCKET_ELEMS = 1 << 22  # 16 MiB of fp32 per bucket
 
 
 class _Bucket:
-    __slots__ = ("index", "params", "flat_param", "flat_grad", "grad_shard", "slots", "shard",
-                 "master", "tl", "ready", "event", "done", "leader", "pending")
+    __slots__ = ("index", "params", "offsets", "flat_param", "flat_grad", "grad_shard", "slots",
+                 "shard", "master", "tl", "ready", "event", "done", "leader", "pending")
 
     def __init__(self, index):
         self.index = index
@@ -86,15 +88,22 @@ class DataParallelFusion:
             if self.mixed and any(p.master is None for p in b.params):
                 raise ConfigError("master weights: every parameter needs an fp32 master")
             mdt = torch.float32 if self.mixed else dt
-            n = sum(p.value.numel() for p in b.params)
+            # every parameter starts on a 128-byte boundary of the flat buffers:
+            # cuDNN/cuBLAS pick their kernels (and so their rounding) by operand
+            # alignment, and a view at an odd bf16 offset would change both
+            align = max(1, 128 // torch.empty((), dtype=dt).element_size())
+            b.offsets = []
+            n = 0
+            for p in b.params:
+                b.offsets.append(n)
+                n += -(-p.value.numel() // align) * align
             padded = -(-n // unit) * unit
             S = padded // self.world
             b.flat_param = torch.zeros(padded, dtype=dt, device=self.device)
             b.flat_grad = torch.zeros(padded, dtype=dt, device=self.device)
             flat_master = torch.zeros(padded, dtype=mdt, device=self.device) if self.mixed else None
-            off = 0
             with torch.no_grad():
-                for p in b.params:
+                for p, off in zip(b.params, b.offsets):
                     v = p.value
                     if not v.is_contiguous():
                         raise ConfigError(f"parameter {p.id} must be contiguous for data parallel")
@@ -104,7 +113,6 @@ class DataParallelFusion:
                         flat_master[off:off + k].copy_(p.master.reshape(-1))
                     v.data = b.flat_param[off:off + k].view_as(v)
                     v.grad = b.flat_grad[off:off + k].view_as(v)
-                    off += k
             if self.mixed:
                 dist.broadcast(flat_master, src=src, group=group)
                 with torch.no_grad():
@@ -164,7 +172,8 @@ class DataParallelFusion:
                 b.grad_shard.mul_(1.0 / self.world)
                 self.update_fn(b.flat_param[b.shard], b.grad_shard, b.slots, t)
         else:
-            kernels.policy_step(b.tl, self.policy._hparams(t), self.scale, self.flags, None)
+            kernels.policy_step(b.tl, self.policy._hparams(t), self.scale,
+                                self.flags | self.policy.device_step_flag, None)
         dist.all_gather_into_tensor(b.flat_param, b.flat_param[b.shard], group=self.group)
 
     def _on_stream(self, stream):

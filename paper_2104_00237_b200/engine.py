@@ -64,14 +64,18 @@ def launch_groups(graph, bucket_elems: int = 0) -> list:
 
 
 class FusionEngine:
-    def __init__(self, graph, policy, side_stream: bool, bucket_elems: int = 0):
+    def __init__(self, graph, policy, side_stream: bool, bucket_elems: int = 0,
+                 priority: str = "high"):
         m = native_engine_module()
         self.graph = graph
         self.kind = policy.kind
         self.side = side_stream
         self.bucket_elems = bucket_elems
         self.groups = launch_groups(graph, bucket_elems)
-        self.stream = torch.cuda.Stream(priority=-1) if side_stream else None
+        # CUDA stream priorities: lower number = higher priority (-1 is the
+        # highest torch exposes, 0 the default)
+        self.stream = (torch.cuda.Stream(priority=-1 if priority == "high" else 0)
+                       if side_stream else None)
         params = graph.parameters
         # history slots exist before the engine captures their pointers
         policy.prepare_history(params)
@@ -91,17 +95,22 @@ class FusionEngine:
     def configure(self, policy, step_t: int, grad_scale=None, max_ctas: int = 0) -> None:
         """Hyper-parameters (and the frozen step index) of the next launches.
         ``max_ctas`` caps each update's grid (0: fill the GPU)."""
+        ds = policy._dstep
         key = (step_t, policy.kind, policy.eta, policy.alpha, policy.weight_decay, policy.epsilon,
-               policy.beta1, policy.beta2, policy.rho, policy.grad_reset, id(grad_scale), max_ctas)
+               policy.beta1, policy.beta2, policy.rho, policy.grad_reset, id(grad_scale), max_ctas,
+               id(ds))
         if key == self._hp_key:
             return
         hp = kernels.hparams(policy.kind, policy.eta, policy.alpha, policy.weight_decay,
                              policy.epsilon, policy.beta1, policy.beta2, policy.rho, step_t)
         zero = policy.grad_reset == "zero"
-        flags = (nat.OF_FLAG_ZERO_GRAD if zero else 0) | (nat.OF_FLAG_SHADOW_BF16 if self.mixed else 0)
+        flags = ((nat.OF_FLAG_ZERO_GRAD if zero else 0) | (nat.OF_FLAG_SHADOW_BF16 if self.mixed else 0)
+                 | policy.device_step_flag)
         self.native.set_hparams(hp.kind, hp.eta, hp.alpha, hp.weight_decay, hp.epsilon, hp.beta1,
                                 hp.beta2, hp.rho, hp.bias_correction1, hp.bias_correction2,
-                                flags, not zero, grad_scale, max_ctas)
+                                flags, not zero, grad_scale, max_ctas,
+                                ds.offset if ds is not None else None,
+                                ds.table if ds is not None else None, step_t)
         self._hp_key = key
 
     @property

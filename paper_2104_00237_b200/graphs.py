@@ -10,16 +10,23 @@ node depends on exactly the events the engine recorded at its issue point
 (gradient-ready for backward fusion, the preceding layer for forward fusion),
 so replay runs the same DAG with no host in the loop.
 
-Constraints (checked): the policy's hyper-parameters must not change between
-replays -- kinds whose update depends on the step index (adam, adamw bias
-corrections) are rejected -- and inputs are copied into static buffers.
+Step-dependent policies (adam, adamw: the bias corrections change every
+iteration) are captured with OF_FLAG_DEVICE_STEP: the graph's first node
+advances a device step offset, and every captured update reads its step index
+as (host index at capture + offset) from a table of the host's own bias
+corrections, so replay j is bit-identical to eager iteration t_capture + j.
+The host policy's ``t`` (and a forward-fusion graph's ``pending_step_t``) is
+advanced per replay so that flushes and checkpoints after replays see the
+right step; stepping the policy eagerly between replays is rejected.
+
+Constraint: inputs are copied into static buffers.
 """
 
 from __future__ import annotations
 
 import torch
 
-from .errors import ConfigError
+from .errors import StateError
 
 _STEP_INDEPENDENT = ("sgd", "sgd-momentum", "adagrad", "rmsprop", "adadelta")
 
@@ -27,16 +34,18 @@ _STEP_INDEPENDENT = ("sgd", "sgd-momentum", "adagrad", "rmsprop", "adadelta")
 class CapturedStep:
     """``step_fn(inputs) -> loss`` captured once, replayed by ``__call__``.
 
-    ``static_inputs`` is a tensor or tuple of tensors on the device; each call
-    copies the given inputs into them (``non_blocking``) before replay.
+    ``static_inputs`` is a tensor or (nested) tuple of tensors on the device;
+    each call copies the given inputs into them (``non_blocking``) before
+    replay.  ``policy``: the OptimizerPolicy the step drives (needed for
+    step-dependent kinds); ``graph``: the Graph (keeps its forward-fusion
+    ``pending_step_t`` in step with the replays).
     """
 
-    def __init__(self, step_fn, static_inputs, policy=None, warmup: int = 3):
-        if policy is not None and policy.kind not in _STEP_INDEPENDENT:
-            raise ConfigError(f"{policy.kind!r} depends on the step index; it cannot be "
-                              "replayed from a captured graph with fixed hyper-parameters")
+    def __init__(self, step_fn, static_inputs, policy=None, warmup: int = 3, graph=None):
         self.static = static_inputs if isinstance(static_inputs, tuple) else (static_inputs,)
         self.step_fn = step_fn
+        self.policy = policy
+        self.owner = graph
         cur = torch.cuda.current_stream()
         side = torch.cuda.Stream()
         side.wait_stream(cur)
@@ -45,21 +54,58 @@ class CapturedStep:
                 step_fn(self._arg())
         cur.wait_stream(side)
         torch.cuda.synchronize()
-        from . import _native
+        from . import _native, kernels
+        self.dstep = None
+        if policy is not None and policy.kind not in _STEP_INDEPENDENT:
+            self.dstep = policy.device_step(torch.device("cuda", torch.cuda.current_device()))
+            self.dstep.ensure(policy.t + 1)
+            torch.cuda.synchronize()
         n0 = _native.launch_count()
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
-            self.loss = step_fn(self._arg())
+            if self.dstep is not None:
+                kernels.step_advance(self.dstep.offset, 1)   # first node of every replay
+                policy._dstep = self.dstep
+                try:
+                    self.loss = step_fn(self._arg())
+                finally:
+                    policy._dstep = None
+            else:
+                self.loss = step_fn(self._arg())
         # liboptfuse_b200 kernel nodes in the graph (each replay launches them all)
         self.native_launches = _native.launch_count() - n0
+        if self.dstep is not None:
+            self.dstep.offset.fill_(-1)     # replay j runs with offset j
+        self.replays = 0
+        self._t = policy.t if policy is not None else None
 
     def _arg(self):
         return self.static if len(self.static) > 1 else self.static[0]
 
     def __call__(self, inputs=None):
+        pol = self.policy
+        if pol is not None:
+            if pol.t != self._t:
+                raise StateError("the policy was stepped outside this captured graph; "
+                                 "capture again to continue with replays")
+            if self.replays > 0:      # the capture's own iteration never ran: replay 0 is t_capture
+                pol.t += 1
+                self._t = pol.t
+                if self.owner is not None and self.owner.pending_step_t is not None:
+                    self.owner.pending_step_t = pol.t
+            if self.dstep is not None:
+                self.dstep.ensure(pol.t + 1)
         if inputs is not None:
             src = inputs if isinstance(inputs, tuple) else (inputs,)
-            for dst, s in zip(self.static, src):
-                dst.copy_(s, non_blocking=True)
+            _copy_into(self.static, src)
         self.graph.replay()
+        self.replays += 1
         return self.loss
+
+
+def _copy_into(dst, src) -> None:
+    for d, s in zip(dst, src):
+        if isinstance(d, (tuple, list)):
+            _copy_into(d, s)
+        else:
+            d.copy_(s, non_blocking=True)

@@ -62,14 +62,29 @@ class TensorList:
 
 
 def hparams(kind: str, eta: float, alpha: float, weight_decay: float, epsilon: float,
-            beta1: float, beta2: float, rho: float, t: int, max_ctas: int = 0) -> nat.OfHparams:
-    """of_hparams for step index t; bias corrections in double (optim.py:145-146)."""
+            beta1: float, beta2: float, rho: float, t: int, max_ctas: int = 0,
+            device_step=None) -> nat.OfHparams:
+    """of_hparams for step index t; bias corrections in double (optim.py:145-146).
+    ``device_step`` (a DeviceStep): fill the OF_FLAG_DEVICE_STEP fields, with
+    t as the base index the device offset is added to."""
     bc1 = bc2 = 1.0
     if kind in ("adam", "adamw"):
         bc1 = 1 - beta1 ** t
         bc2 = 1 - beta2 ** t
-    return nat.OfHparams(nat.KIND_CODES[kind], max_ctas, eta, alpha, weight_decay, epsilon,
-                         beta1, beta2, rho, bc1, bc2)
+    hp = nat.OfHparams(nat.KIND_CODES[kind], max_ctas, eta, alpha, weight_decay, epsilon,
+                       beta1, beta2, rho, bc1, bc2)
+    if device_step is not None:
+        hp.step_offset_dev = device_step.offset.data_ptr()
+        hp.step_table_dev = device_step.table.data_ptr()
+        hp.step_table_rows = device_step.table.shape[0]
+        hp.t_base = t
+    return hp
+
+
+def step_advance(offset: torch.Tensor, delta: int = 1, stream=None) -> None:
+    """of_step_advance: offset += delta on the device (stream-ordered)."""
+    st = nat.lib().of_step_advance(offset.data_ptr(), int(delta), _handle(stream))
+    nat.check(st, "of_step_advance")
 
 
 def policy_step(tl: TensorList, hp: nat.OfHparams, grad_scale, flags: int, stream) -> None:

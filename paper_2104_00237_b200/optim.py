@@ -72,6 +72,8 @@ class OptimizerPolicy:
     grad_reset: str = "zero"
     _lists: dict = field(default_factory=dict, repr=False, compare=False)
     _hp_cache: tuple = field(default=(None, None), repr=False, compare=False)
+    _dstep_buf: object = field(default=None, repr=False, compare=False)
+    _dstep: object = field(default=None, repr=False, compare=False)   # active while capturing
 
     def __post_init__(self):
         if self.kind not in KINDS:
@@ -164,7 +166,8 @@ class OptimizerPolicy:
                 tl.set(i, v, v.grad, h[s_a] if s_a else None, h[s_b] if s_b else None, None)
         p0 = params[0]
         tl.set_dtypes(p0.master.dtype if mixed else p0.value.dtype, p0.value.grad.dtype)
-        flags = (nat.OF_FLAG_ZERO_GRAD if zero else 0) | (nat.OF_FLAG_SHADOW_BF16 if mixed else 0)
+        flags = ((nat.OF_FLAG_ZERO_GRAD if zero else 0) | (nat.OF_FLAG_SHADOW_BF16 if mixed else 0)
+                 | self.device_step_flag)
         kernels.policy_step(tl, self._hparams(t), scale, flags, stream)
         if trace is not None:
             for p in params:
@@ -205,13 +208,28 @@ class OptimizerPolicy:
                     if name not in h:
                         h[name] = torch.zeros_like(ref, memory_format=torch.preserve_format)
 
+    # -- CUDA-graph replay of step-dependent kinds ----------------------------
+
+    @property
+    def device_step_flag(self) -> int:
+        """OF_FLAG_DEVICE_STEP while a CUDA graph is being captured."""
+        return nat.OF_FLAG_DEVICE_STEP if self._dstep is not None else 0
+
+    def device_step(self, device) -> "DeviceStep":
+        """The device-resident step index of this policy (created on first use)."""
+        ds = self._dstep_buf
+        if ds is None or ds.betas != (self.beta1, self.beta2):
+            ds = DeviceStep(self, device)
+            self._dstep_buf = ds
+        return ds
+
     def _hparams(self, t: int) -> nat.OfHparams:
         key = (t, self.kind, self.eta, self.alpha, self.weight_decay, self.epsilon,
-               self.beta1, self.beta2, self.rho)
+               self.beta1, self.beta2, self.rho, id(self._dstep))
         cached_key, hp = self._hp_cache
         if cached_key != key:
             hp = kernels.hparams(self.kind, self.eta, self.alpha, self.weight_decay, self.epsilon,
-                                 self.beta1, self.beta2, self.rho, t)
+                                 self.beta1, self.beta2, self.rho, t, device_step=self._dstep)
             self._hp_cache = (key, hp)
         return hp
 
@@ -224,6 +242,40 @@ def bytes_per_element(kind: str, param_itemsize: int = 4, grad_itemsize: int | N
     slots = len(_HISTORY_SLOTS[kind])
     g = param_itemsize if grad_itemsize is None else grad_itemsize
     return param_itemsize * (2 + 2 * slots) + g + (2 if shadow else 0)
+
+
+class DeviceStep:
+    """Device-resident step index for CUDA-graph replay (OF_FLAG_DEVICE_STEP).
+
+    A captured launch reads its step index as ``t_base + offset`` when it runs,
+    where ``t_base`` is the host step index at capture and ``offset`` (one
+    device int64) is advanced by the graph's first node on every replay; the
+    Adam bias corrections come from ``table[t] = (1 - beta1**t, 1 - beta2**t)``,
+    filled on the host with the very Python expressions of optim.py:145-146, so
+    a replayed step is bit-identical to the eager one.  The table is allocated
+    once (its address is baked into the graph) and filled ahead of use."""
+
+    ROWS = 1 << 20      # 16 MiB: a million replayed iterations
+    CHUNK = 4096
+
+    def __init__(self, policy, device):
+        self.betas = (policy.beta1, policy.beta2)
+        self.offset = torch.zeros(1, dtype=torch.int64, device=device)
+        self.table = torch.zeros((self.ROWS, 2), dtype=torch.float64, device=device)
+        self.filled = 0
+        self.ensure(policy.t + 1)
+
+    def ensure(self, t: int) -> None:
+        """Rows up to index ``t`` are valid (stream-ordered host copy)."""
+        if t < self.filled:
+            return
+        if t >= self.ROWS:
+            raise StateError(f"step index {t} beyond the device step table ({self.ROWS} rows)")
+        hi = min(self.ROWS, max(t + 1, self.filled + self.CHUNK))
+        b1, b2 = self.betas
+        rows = [(1 - b1 ** k, 1 - b2 ** k) for k in range(self.filled, hi)]
+        self.table[self.filled:hi].copy_(torch.tensor(rows, dtype=torch.float64))
+        self.filled = hi
 
 
 def algorithmic_bytes(kind: str, params) -> int:

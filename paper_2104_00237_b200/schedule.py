@@ -161,12 +161,13 @@ class _TraceRecorder:
                     self.steps_for_group(gi)
 
 
-def _engine(graph: Graph, policy: OptimizerPolicy, side: bool, bucket_elems: int = 0):
+def _engine(graph: Graph, policy: OptimizerPolicy, side: bool, bucket_elems: int = 0,
+            priority: str = "high"):
     from .engine import FusionEngine
-    key = (policy.kind, side, bucket_elems)
+    key = (policy.kind, side, bucket_elems) + (() if priority == "high" else (priority,))
     eng = graph._engines.get(key)
     if eng is None:
-        eng = FusionEngine(graph, policy, side, bucket_elems)
+        eng = FusionEngine(graph, policy, side, bucket_elems, priority)
         graph._engines[key] = eng
     return eng
 
@@ -393,7 +394,8 @@ def default_update_ctas() -> int:
 
 def run_backward_fusion(graph: Graph, policy: OptimizerPolicy, inp, workers: int = 1, *,
                         timing: bool = True, trace: bool = False,
-                        bucket_elems: int = 0, update_ctas: int | None = None) -> StepReport:
+                        bucket_elems: int = 0, update_ctas: int | None = None,
+                        update_priority: str = "high") -> StepReport:
     """Eager schedule: update each layer as soon as its gradients are complete.
 
     ``workers=1`` issues each update inline on the autograd stream;
@@ -402,7 +404,10 @@ def run_backward_fusion(graph: Graph, policy: OptimizerPolicy, inp, workers: int
     the preceding layers; ``update_ctas`` optionally caps each update's grid
     so it streams alongside the backward (default 0: uncapped).
     ``bucket_elems`` merges consecutive layers (backward order) into launch
-    groups of at least that many elements.
+    groups of at least that many elements.  ``update_priority`` ("high" |
+    "low") is the side stream's priority: high mirrors the reference runner's
+    step-first heap; low lets a GPU-bound backward keep the SMs and the
+    updates fill the gaps.
     Raises GlobalInfoRequired, mutating nothing, for policies or transforms
     that must see all gradients first (schedule.py:174-177).
     """
@@ -416,8 +421,11 @@ def run_backward_fusion(graph: Graph, policy: OptimizerPolicy, inp, workers: int
         raise ConfigError(f"workers must be >= 1, got {workers}")
     if bucket_elems < 0:
         raise ConfigError(f"bucket_elems must be >= 0, got {bucket_elems}")
+    if update_priority not in ("high", "low"):
+        raise ConfigError(f"update_priority must be 'high' or 'low', got {update_priority!r}")
     _leave_forward_fusion(graph, policy)
-    eng = _engine(graph, policy, workers > 1, bucket_elems)
+    eng = _engine(graph, policy, workers > 1, bucket_elems,
+                  update_priority if workers > 1 else "high")
     policy.begin_iteration()
     if workers > 1 and update_ctas is None:
         update_ctas = default_update_ctas()

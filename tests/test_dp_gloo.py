@@ -121,7 +121,8 @@ def _worker_mixed(rank, world, port, schedule, out):
             run(x.to(torch.bfloat16))
         dp.flush()
         flat = torch.cat([p.value.detach().reshape(-1) for p in g.parameters])
-        shards = [(b.master.numpy().copy(), [p.id for p in b.params]) for b in dp.buckets]
+        shards = [(b.master.numpy().copy(), [p.id for p in b.params], list(b.offsets))
+                  for b in dp.buckets]
         out[rank] = (flat.view(torch.int16).numpy().tobytes(), shards)
     finally:
         dist.destroy_process_group()
@@ -167,9 +168,12 @@ def test_sharded_mixed_precision_equals_single_process(schedule):
     assert out[0][0] == want_bf16
     # each rank owns one shard of every bucket's fp32 master: stitch rank 0 +
     # rank 1 per bucket and compare with the reference masters bit for bit
-    for (s0, ids), (s1, ids1) in zip(out[0][1], out[1][1]):
+    for (s0, ids, offs), (s1, ids1, _) in zip(out[0][1], out[1][1]):
         assert ids == ids1
         full = np.concatenate([s0, s1])
-        want = np.concatenate([want_master[i] for i in ids])
-        assert full[:want.size].tobytes() == want.tobytes()
-        assert not full[want.size:].any()     # padding stays zero
+        mask = np.ones(full.size, bool)
+        for i, off in zip(ids, offs):
+            w = want_master[i]
+            assert full[off:off + w.size].tobytes() == w.tobytes()
+            mask[off:off + w.size] = False
+        assert not full[mask].any()     # alignment gaps and padding stay zero

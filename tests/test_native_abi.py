@@ -28,7 +28,7 @@ def test_library_exports_every_symbol():
     so = nat.lib()
     for name in declared_symbols():
         assert hasattr(so, name), name
-    assert so.of_abi_version() == 1
+    assert so.of_abi_version() == nat.ABI_VERSION == 2
     assert so.of_status_string(0) == b"ok"
     assert so.of_sqnorm_workspace_len() >= 148
 
@@ -68,6 +68,15 @@ def test_invalid_arguments_rejected_before_launch():
     tl.state1[0] = 0x4000
     assert so.of_policy_step_mt(tl.ref, ctypes.byref(adam), None, 0, None) == nat.OF_ERR_INVALID
     assert b"bias" in so.of_last_error()
+    # OF_FLAG_DEVICE_STEP needs the device offset and table (and ignores the
+    # host bias corrections, which are zero here)
+    dev = nat.OF_FLAG_DEVICE_STEP
+    assert so.of_policy_step_mt(tl.ref, ctypes.byref(adam), None, dev, None) == nat.OF_ERR_INVALID
+    assert b"DEVICE_STEP" in so.of_last_error()
+    adam.step_offset_dev, adam.step_table_dev, adam.step_table_rows = 0x5000, 0x6000, 1
+    assert so.of_policy_step_mt(tl.ref, ctypes.byref(adam), None, dev, None) == nat.OF_ERR_INVALID
+    assert b"rows" in so.of_last_error()
+    assert so.of_step_advance(None, 1, None) == nat.OF_ERR_INVALID
     empty = kernels.TensorList(0)
     assert so.of_policy_step_mt(empty.ref, ctypes.byref(hp), None, 0, None) == nat.OF_OK
     assert so.of_clip_coef(None, 1.0, None, None, None) == nat.OF_ERR_INVALID
