@@ -2,8 +2,9 @@
 
 Accepts the reference CLI's flags (/root/reference/pkg/src/optfuse/cli.py:22-49)
 so existing sweep scripts run unchanged, plus the B200 knobs
-(``--bucket-elems``, ``--grad-reset``, ``--device``) and the benchmark CNNs as
-``--model`` choices.  Exit status: 2 for a configuration error, 1 when the
+(``--bucket-elems``, ``--grad-reset``, ``--device``, ``--dtype``) and the
+benchmark networks (the BASELINE.json CNNs and ``bert_base``) as ``--model``
+choices.  Multi-GPU runs go through ``bench.py`` under torchrun.  Exit status: 2 for a configuration error, 1 when the
 verify grid finds a mismatch, 0 otherwise.
 """
 
@@ -50,6 +51,8 @@ _OPTIONS = (
                                             help="launch groups of >= this many elements")),
     ("--grad-reset", "grad_reset", dict(default="zero", choices=("zero", "none"))),
     ("--device", "device", dict(default="cuda")),
+    ("--dtype", "dtype", dict(default="fp32", choices=("fp32", "bf16"),
+                              help="bf16: bf16 module with fp32 master weights (networks only)")),
 )
 
 

@@ -19,7 +19,9 @@ The host policy's ``t`` (and a forward-fusion graph's ``pending_step_t``) is
 advanced per replay so that flushes and checkpoints after replays see the
 right step; stepping the policy eagerly between replays is rejected.
 
-Constraint: inputs are copied into static buffers.
+Constraints: inputs are copied into static buffers; a forward-fusion step
+must be captured with ``graph=`` so that its gradients can be kept resident
+across replays (``grad_reset`` is switched to "zero" for it, see __init__).
 """
 
 from __future__ import annotations
@@ -54,6 +56,18 @@ class CapturedStep:
                 step_fn(self._arg())
         cur.wait_stream(side)
         torch.cuda.synchronize()
+        # Forward fusion reads, in iteration i+1, the gradients iteration i
+        # produced.  Released gradients (grad_reset="none") would be
+        # re-allocated at other addresses by the next backward, and a replay
+        # would read the captured (stale) ones; keeping them allocated and
+        # zeroed in the update kernel makes the buffers the graph captured the
+        # ones every replay writes and reads.
+        self.grad_reset_forced = False
+        owner = getattr(graph, "_flag_owner", None)
+        if (policy is not None and policy.grad_reset == "none" and owner is not None
+                and owner.num_pending() > 0):
+            policy.grad_reset = "zero"
+            self.grad_reset_forced = True
         from . import _native, kernels
         self.dstep = None
         if policy is not None and policy.kind not in _STEP_INDEPENDENT:

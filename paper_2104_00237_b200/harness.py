@@ -38,7 +38,7 @@ STAGES = ("forward", "backward", "optimizer")
 LOCAL_OPTIMIZERS = ("sgd", "sgd-momentum", "adagrad", "rmsprop", "adadelta", "adam")
 CSV_HEADER = "\t".join(("idx", FORWARD_FUSION, BACKWARD_FUSION))
 SKIP_MARKER = "skip"
-MODEL_CHOICES = models.SYNTHETIC + tuple(models.CLASSIFIERS)
+MODEL_CHOICES = models.SYNTHETIC + tuple(models.CLASSIFIERS) + tuple(models.NETWORKS)
 VERIFY_MODELS = (("chain", dict(layers=3, width=4)), ("shared-chain", dict(layers=4, width=4)),
                  ("mul-probe", dict(width=3)))
 _RUNNERS = {BASELINE: run_baseline, FORWARD_FUSION: run_forward_fusion,
@@ -70,6 +70,7 @@ class BenchConfig:
     bucket_elems: int = 0
     grad_reset: str = "zero"
     device: str = "cuda"
+    dtype: str = "fp32"
 
     def __post_init__(self):
         checks = (
@@ -80,6 +81,9 @@ class BenchConfig:
             (self.warmup >= 0, f"warmup must be >= 0, got {self.warmup}"),
             (self.batch >= 1, f"batch must be >= 1, got {self.batch}"),
             (self.metric in ("speedup", "saved"), f"metric must be speedup|saved, got {self.metric!r}"),
+            (self.dtype in ("fp32", "bf16"), f"dtype must be fp32|bf16, got {self.dtype!r}"),
+            (self.dtype == "fp32" or self.model not in models.SYNTHETIC,
+             "--dtype bf16 (bf16 module + fp32 master weights) is for the benchmark networks"),
             (self.batch_sweep is None or 1 <= self.batch_sweep[0] <= self.batch_sweep[1],
              f"batch sweep needs 1 <= lo <= hi, got {self.batch_sweep}"),
         )
@@ -105,10 +109,14 @@ class _Session:
             self.inp = models.make_input(self.graph, batch, cfg.seed)
         else:
             if cfg.precision != "f32":
-                raise ConfigError("the benchmark CNNs run in f32")
+                raise ConfigError("the benchmark networks run in f32 (or --dtype bf16)")
             self.graph = models.build_classifier(cfg.model, device=cfg.device, seed=cfg.seed)
             self.graph.track_counts = False
             self.inp = models.synthetic_batch(cfg.model, batch, device=cfg.device, seed=cfg.seed)
+            if cfg.dtype == "bf16":   # bf16 module, fp32 masters updated in the same pass
+                self.graph.use_master_weights()
+                x, y = self.inp
+                self.inp = (x.to(torch.bfloat16) if x.is_floating_point() else x, y)
         self.policy = OptimizerPolicy(kind=cfg.optimizer, eta=cfg.eta,
                                       weight_decay=cfg.weight_decay, clip_norm=cfg.clip_norm,
                                       grad_reset=cfg.grad_reset)

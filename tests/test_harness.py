@@ -22,7 +22,8 @@ def test_cli_accepts_every_reference_flag():
 
 @pytest.mark.parametrize("kw", [dict(mode="plot"), dict(schedule="lazy"), dict(iters=0),
                                 dict(warmup=-1), dict(batch=0), dict(metric="ratio"),
-                                dict(batch_sweep=(3, 1)), dict(model="resnet152")])
+                                dict(batch_sweep=(3, 1)), dict(model="resnet152"),
+                                dict(dtype="fp16"), dict(model="chain", dtype="bf16")])
 def test_config_validation(kw):
     with pytest.raises(ConfigError):
         harness.BenchConfig(**kw)
@@ -84,3 +85,13 @@ def test_cli_time_mode_on_a_cnn():
     keys = [ln.split("=")[0] for ln in proc.stdout.split()]
     assert keys == ["forward_ms", "backward_ms", "optimizer_ms", "total_ms", "median_ms",
                     "baseline_total_ms", "speedup"]
+
+
+@pytest.mark.gpu
+def test_cli_bf16_master_weights_on_a_cnn():
+    proc = subprocess.run([sys.executable, "-m", "paper_2104_00237_b200.cli", "--model",
+                           "resnet18_cifar", "--optimizer", "adamw", "--batch", "16", "--dtype", "bf16",
+                           "--iters", "3", "--warmup", "2", "--workers", "2", "--mode", "breakdown"],
+                          capture_output=True, text=True, timeout=600)
+    assert proc.returncode == 0, proc.stderr
+    assert "backward-fusion" in proc.stdout

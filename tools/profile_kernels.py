@@ -3,6 +3,7 @@
     python tools/profile_kernels.py bf      # MobileNetV2 b128 backward fusion, bucketed launches
     python tools/profile_kernels.py vgg     # one multi-tensor Adam launch over VGG-16 (138 M params)
     python tools/profile_kernels.py bert    # one AdamW launch over BERT-base (206 tensors, 110 M)
+    python tools/profile_kernels.py r50mixed  # ResNet-50 bf16 + fp32 masters, AdamW, one launch
 """
 
 import sys
@@ -27,8 +28,10 @@ def bf(iters=6):
     torch.cuda.synchronize()
 
 
-def vgg(iters=3, model="vgg16", kind="adam"):
+def vgg(iters=3, model="vgg16", kind="adam", mixed=False):
     g = of.build_classifier(model, device="cuda")
+    if mixed:
+        g.use_master_weights()
     pol = of.OptimizerPolicy(kind, eta=1e-4, grad_reset="none")
     for p in g.parameters:
         p.value.grad = torch.randn_like(p.value) * 0.01
@@ -45,5 +48,9 @@ def bert(iters=3):
     vgg(iters, "bert_base", "adamw")
 
 
+def r50mixed(iters=3):
+    vgg(iters, "resnet50", "adamw", mixed=True)
+
+
 if __name__ == "__main__":
-    {"bf": bf, "vgg": vgg, "bert": bert}[sys.argv[1]]()
+    {"bf": bf, "vgg": vgg, "bert": bert, "r50mixed": r50mixed}[sys.argv[1]]()
