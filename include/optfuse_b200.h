@@ -151,6 +151,38 @@ int of_adam_mt(const of_tensor_list* list, double eta, double beta1, double beta
  * launches once per replay. */
 int of_step_advance(int64_t* step_offset_dev, int64_t delta, void* stream);
 
+/* ---- Data parallel over peer memory (NVLink / NVSwitch) ----------------
+ * One bucket of a data-parallel model: every rank holds a flat gradient and a
+ * flat parameter buffer of the same padded size, mapped into every peer's
+ * address space (e.g. torch symmetric memory).  Rank r owns the elements
+ * [shard_begin, shard_begin + shard_len) and their optimizer history. */
+#define OF_MAX_PEERS 16
+
+typedef struct of_peer_bucket {
+  int32_t world;           /* W, 1 .. OF_MAX_PEERS */
+  int32_t rank;            /* this rank */
+  int32_t param_dtype;     /* OF_F32 / OF_F64, or OF_BF16 with an fp32 master shard */
+  int32_t grad_dtype;      /* same as param_dtype */
+  void* const* peer_grad;  /* [W] flat gradient buffers, as mapped on this GPU */
+  void* const* peer_param; /* [W] flat parameter buffers, as mapped on this GPU */
+  void* master;            /* OF_BF16: fp32 master of the shard; else NULL */
+  void* state0;            /* history of the shard (optim.py:24-31 slots) */
+  void* state1;
+  int64_t shard_begin;     /* multiple of 4 */
+  int64_t shard_len;       /* multiple of 4 */
+} of_peer_bucket;
+
+/* Reduce-scatter + policy step + all-gather of one bucket in ONE kernel: sums
+ * the shard's gradients over the W peers (rank order), multiplies by
+ * *grad_scale_dev (1/W; NULL = 1), applies OptimizerPolicy.step to the shard
+ * (optim.py:74-148, same arithmetic as of_policy_step_mt), writes the new
+ * parameter (bf16 rounding of the master for OF_BF16) into every peer's
+ * parameter buffer and zeroes the shard's gradient in every peer.  The caller
+ * orders it with a cross-rank barrier before (all gradients complete) and
+ * after (all writes landed).  flags: 0 or OF_FLAG_DEVICE_STEP. */
+int of_dp_step_peer(const of_peer_bucket* bucket, const of_hparams* hp,
+                    const float* grad_scale_dev, uint32_t flags, void* stream);
+
 /* Sum of squares of every grad in `list`, accumulated in f64 with a fixed
  * (deterministic) reduction order (optim.py:160-164).  Uses `workspace_dev`
  * (>= of_sqnorm_workspace_len() doubles).  Writes *out_dev = sum, or

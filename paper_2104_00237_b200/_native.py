@@ -29,7 +29,7 @@ KIND_CODES = {"sgd": 0, "sgd-momentum": 1, "adagrad": 2, "rmsprop": 3, "adadelta
 
 # every symbol include/optfuse_b200.h declares (checked by tests/test_native_abi.py)
 SYMBOLS = ("of_abi_version", "of_status_string", "of_last_error", "of_launch_count",
-           "of_policy_step_mt", "of_sgdm_mt", "of_adam_mt", "of_step_advance",
+           "of_policy_step_mt", "of_sgdm_mt", "of_adam_mt", "of_step_advance", "of_dp_step_peer",
            "of_sqnorm_workspace_len", "of_sqnorm_mt", "of_clip_coef")
 
 _vp = ctypes.c_void_p
@@ -51,6 +51,17 @@ class OfTensorList(ctypes.Structure):
                 ("grad_dtype", ctypes.c_int32), ("reserved", ctypes.c_int32),
                 ("param", _PP), ("grad", _PP), ("state0", _PP), ("state1", _PP),
                 ("shadow", _PP), ("numel", ctypes.POINTER(ctypes.c_int64))]
+
+
+OF_MAX_PEERS = 16
+
+
+class OfPeerBucket(ctypes.Structure):
+    _fields_ = [("world", ctypes.c_int32), ("rank", ctypes.c_int32),
+                ("param_dtype", ctypes.c_int32), ("grad_dtype", ctypes.c_int32),
+                ("peer_grad", _PP), ("peer_param", _PP), ("master", _vp),
+                ("state0", _vp), ("state1", _vp),
+                ("shard_begin", ctypes.c_int64), ("shard_len", ctypes.c_int64)]
 
 
 _lib = None
@@ -86,6 +97,9 @@ def lib():
         ctypes.c_int, _vp, ctypes.c_uint32, _vp]
     so.of_step_advance.restype = ctypes.c_int
     so.of_step_advance.argtypes = [_vp, ctypes.c_int64, _vp]
+    so.of_dp_step_peer.restype = ctypes.c_int
+    so.of_dp_step_peer.argtypes = [ctypes.POINTER(OfPeerBucket), ctypes.POINTER(OfHparams), _vp,
+                                   ctypes.c_uint32, _vp]
     so.of_sqnorm_workspace_len.restype = ctypes.c_int64
     so.of_sqnorm_mt.restype = ctypes.c_int
     so.of_sqnorm_mt.argtypes = [ctypes.POINTER(OfTensorList), _vp, ctypes.c_int64, _vp,

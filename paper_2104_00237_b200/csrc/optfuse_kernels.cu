@@ -567,56 +567,142 @@ CoupledWd<T> coupled(const of_hparams* hp) {
   return CoupledWd<T>{static_cast<T>(hp->weight_decay), hp->weight_decay > 0.0};
 }
 
-template <class T, class G>
-int dispatch_kind(const of_tensor_list* l, const of_hparams* hp, const float* gscale,
-                  uint32_t flags, cudaStream_t s) {
+// Builds the functor of hp->kind (constants rounded once to T, as numpy does)
+// and hands it to f.
+template <class T, class F>
+int with_op(const of_hparams* hp, F&& f) {
   const T neg_eta = static_cast<T>(-hp->eta);
-  StepSrc step{nullptr, nullptr, 0, 0};
-  if (flags & OF_FLAG_DEVICE_STEP)
-    step = StepSrc{hp->step_offset_dev, hp->step_table_dev, hp->step_table_rows, hp->t_base};
-  flags &= ~OF_FLAG_DEVICE_STEP;
   switch (hp->kind) {
-    case OF_SGD: {
-      SgdOp<T> op{coupled<T>(hp), neg_eta};
-      return launch_step<SgdOp<T>, T, G>(l, op, gscale, flags, step, hp->max_ctas, s);
-    }
-    case OF_SGD_MOMENTUM: {
-      SgdMomentumOp<T> op{coupled<T>(hp), neg_eta, static_cast<T>(hp->alpha)};
-      return launch_step<SgdMomentumOp<T>, T, G>(l, op, gscale, flags, step, hp->max_ctas, s);
-    }
-    case OF_ADAGRAD: {
-      AdagradOp<T> op{coupled<T>(hp), neg_eta, static_cast<T>(hp->epsilon)};
-      return launch_step<AdagradOp<T>, T, G>(l, op, gscale, flags, step, hp->max_ctas, s);
-    }
-    case OF_RMSPROP: {
-      RmspropOp<T> op{coupled<T>(hp), neg_eta, static_cast<T>(hp->epsilon),
-                      static_cast<T>(hp->rho), static_cast<T>(1.0 - hp->rho)};
-      return launch_step<RmspropOp<T>, T, G>(l, op, gscale, flags, step, hp->max_ctas, s);
-    }
-    case OF_ADADELTA: {
-      AdadeltaOp<T> op{coupled<T>(hp), neg_eta, static_cast<T>(hp->epsilon),
-                       static_cast<T>(hp->rho), static_cast<T>(1.0 - hp->rho)};
-      return launch_step<AdadeltaOp<T>, T, G>(l, op, gscale, flags, step, hp->max_ctas, s);
-    }
-    case OF_ADAM: {
-      AdamOp<T> op{coupled<T>(hp), neg_eta, static_cast<T>(hp->epsilon),
-                   static_cast<T>(hp->beta1), static_cast<T>(hp->beta2),
-                   static_cast<T>(1.0 - hp->beta1), static_cast<T>(1.0 - hp->beta2),
-                   static_cast<T>(hp->bias_correction1), static_cast<T>(hp->bias_correction2)};
-      return launch_step<AdamOp<T>, T, G>(l, op, gscale, flags, step, hp->max_ctas, s);
-    }
+    case OF_SGD: return f(SgdOp<T>{coupled<T>(hp), neg_eta});
+    case OF_SGD_MOMENTUM: return f(SgdMomentumOp<T>{coupled<T>(hp), neg_eta, static_cast<T>(hp->alpha)});
+    case OF_ADAGRAD: return f(AdagradOp<T>{coupled<T>(hp), neg_eta, static_cast<T>(hp->epsilon)});
+    case OF_RMSPROP:
+      return f(RmspropOp<T>{coupled<T>(hp), neg_eta, static_cast<T>(hp->epsilon),
+                            static_cast<T>(hp->rho), static_cast<T>(1.0 - hp->rho)});
+    case OF_ADADELTA:
+      return f(AdadeltaOp<T>{coupled<T>(hp), neg_eta, static_cast<T>(hp->epsilon),
+                             static_cast<T>(hp->rho), static_cast<T>(1.0 - hp->rho)});
+    case OF_ADAM:
+      return f(AdamOp<T>{coupled<T>(hp), neg_eta, static_cast<T>(hp->epsilon),
+                         static_cast<T>(hp->beta1), static_cast<T>(hp->beta2),
+                         static_cast<T>(1.0 - hp->beta1), static_cast<T>(1.0 - hp->beta2),
+                         static_cast<T>(hp->bias_correction1), static_cast<T>(hp->bias_correction2)});
     case OF_ADAMW: {
       const double w1 = 1.0 - hp->beta1;
-      AdamWOp<T> op{static_cast<T>(1.0 - hp->eta * hp->weight_decay), static_cast<T>(w1),
-                    static_cast<T>(hp->beta2), static_cast<T>(1.0 - hp->beta2),
-                    static_cast<T>(std::sqrt(hp->bias_correction2)), static_cast<T>(hp->epsilon),
-                    static_cast<T>(-(hp->eta / hp->bias_correction1)),
-                    hp->weight_decay != 0.0, std::fabs(w1) < 0.5, hp->eta};
-      return launch_step<AdamWOp<T>, T, G>(l, op, gscale, flags, step, hp->max_ctas, s);
+      return f(AdamWOp<T>{static_cast<T>(1.0 - hp->eta * hp->weight_decay), static_cast<T>(w1),
+                          static_cast<T>(hp->beta2), static_cast<T>(1.0 - hp->beta2),
+                          static_cast<T>(std::sqrt(hp->bias_correction2)), static_cast<T>(hp->epsilon),
+                          static_cast<T>(-(hp->eta / hp->bias_correction1)),
+                          hp->weight_decay != 0.0, std::fabs(w1) < 0.5, hp->eta});
     }
     default:
       return fail(OF_ERR_INVALID, "unknown optimizer kind %d", hp->kind);
   }
+}
+
+StepSrc step_source(const of_hparams* hp, uint32_t flags) {
+  if (flags & OF_FLAG_DEVICE_STEP)
+    return StepSrc{hp->step_offset_dev, hp->step_table_dev, hp->step_table_rows, hp->t_base};
+  return StepSrc{nullptr, nullptr, 0, 0};
+}
+
+template <class T, class G>
+int dispatch_kind(const of_tensor_list* l, const of_hparams* hp, const float* gscale,
+                  uint32_t flags, cudaStream_t s) {
+  const StepSrc step = step_source(hp, flags);
+  flags &= ~OF_FLAG_DEVICE_STEP;
+  return with_op<T>(hp, [&](auto op) {
+    return launch_step<decltype(op), T, G>(l, op, gscale, flags, step, hp->max_ctas, s);
+  });
+}
+
+// ---------------------------------------------------------------------------
+// Data-parallel fused step over peer memory (NVLink / NVSwitch).
+//
+// Rank r owns the shard [begin, begin + len) of a flat bucket.  One kernel
+// replaces reduce-scatter -> update -> all-gather: each thread loads its
+// gradient vector from every peer's buffer (peer-mapped pointers, fixed rank
+// order, so the sum is deterministic), applies the policy step to the local
+// parameter (or fp32 master) and history, stores the new parameter (or its
+// bf16 shadow) into every peer's parameter buffer and zeroes the gradient
+// vector it read in every peer.  Each gradient element is read and zeroed by
+// exactly one rank (its shard owner), so there is no write-write race; the
+// caller brackets the launch with a cross-rank barrier (gradients complete
+// before, writes visible after).
+// ---------------------------------------------------------------------------
+struct PeerParams {
+  void* grad[OF_MAX_PEERS];
+  void* param[OF_MAX_PEERS];
+  void* master;            // fp32 master shard (mixed) or nullptr
+  void* s0;                // history shards
+  void* s1;
+  int64_t begin, len;      // shard, in elements of the flat buffers (multiples of 4)
+  int32_t world, rank;
+};
+
+template <class Op, class T, class G, bool kMixed>
+__global__ void __launch_bounds__(kThreads)
+peer_step_kernel(const __grid_constant__ PeerParams pp, const Op op_in,
+                 const float* __restrict__ gscale, const StepSrc step) {
+  using GV = typename GradVal<G>::type;
+  Op op = op_in;
+  if (step.offset != nullptr) {
+    int64_t t = step.t_base + *step.offset;
+    t = t < 1 ? 1 : (t >= step.rows ? step.rows - 1 : t);
+    op.set_step(step.table[2 * t], step.table[2 * t + 1]);
+  }
+  const bool has_scale = gscale != nullptr;
+  const T scale = has_scale ? T(*gscale) : T(1);
+  const int64_t nvec = pp.len / kVec;
+  const int W = pp.world;
+  for (int64_t v = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; v < nvec;
+       v += static_cast<int64_t>(gridDim.x) * kThreads) {
+    const int64_t e = pp.begin + kVec * v;   // flat-buffer element
+    const int64_t o = kVec * v;              // shard element
+    GV acc[4], tmp[4];
+    ld4(static_cast<const G*>(pp.grad[0]) + e, acc);
+    for (int w = 1; w < W; ++w) {
+      ld4(static_cast<const G*>(pp.grad[w]) + e, tmp);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc[k] = o_add(acc[k], tmp[k]);
+    }
+    T p[4], a[4], b[4];
+    if (kMixed) ld4(static_cast<const T*>(pp.master) + o, p);
+    else ld4(static_cast<const T*>(pp.param[pp.rank]) + e, p);
+    if (Op::kSlots >= 1) ld4(static_cast<const T*>(pp.s0) + o, a);
+    if (Op::kSlots >= 2) ld4(static_cast<const T*>(pp.s1) + o, b);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      T gk = static_cast<T>(acc[k]);
+      if (has_scale) gk = o_mul(gk, scale);   // 1/W (and the clip factor)
+      op(p[k], gk, a[k], b[k]);
+    }
+    if (Op::kSlots >= 1) st4(static_cast<T*>(pp.s0) + o, a);
+    if (Op::kSlots >= 2) st4(static_cast<T*>(pp.s1) + o, b);
+    if (kMixed) st4(static_cast<T*>(pp.master) + o, p);
+    for (int w = 0; w < W; ++w) {
+      if (kMixed) st4_bf16(static_cast<__nv_bfloat16*>(pp.param[w]) + e, p);
+      else st4(static_cast<T*>(pp.param[w]) + e, p);
+      st4_zero(static_cast<G*>(pp.grad[w]) + e);
+    }
+  }
+}
+
+template <class T, class G, bool kMixed>
+int dispatch_peer(const PeerParams& pp, const of_hparams* hp, const float* gscale, uint32_t flags,
+                  cudaStream_t s) {
+  const StepSrc step = step_source(hp, flags);
+  const int64_t nvec = pp.len / kVec;
+  if (nvec == 0) return OF_OK;
+  int64_t grid = (nvec + kThreads - 1) / kThreads;
+  int64_t cap = static_cast<int64_t>(sm_count()) * kCtasPerSm;
+  if (hp->max_ctas > 0 && hp->max_ctas < cap) cap = hp->max_ctas;
+  if (grid > cap) grid = cap;
+  return with_op<T>(hp, [&](auto op) {
+    peer_step_kernel<decltype(op), T, G, kMixed><<<static_cast<int>(grid), kThreads, 0, s>>>(
+        pp, op, gscale, step);
+    return check_launch("peer_step_kernel");
+  });
 }
 
 template <class G, int CAP>
@@ -771,6 +857,60 @@ int of_clip_coef(const double* sqnorm_dev, double max_norm, float* coef_dev, dou
   if (!(max_norm >= 0.0)) return fail(OF_ERR_INVALID, "max_norm must be >= 0, got %g", max_norm);
   clip_coef_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(sqnorm_dev, max_norm, coef_dev, factor_dev);
   return check_launch("clip_coef_kernel");
+}
+
+int of_dp_step_peer(const of_peer_bucket* b, const of_hparams* hp, const float* grad_scale_dev,
+                    uint32_t flags, void* stream) {
+  g_err[0] = '\0';
+  if (!b || !hp) return fail(OF_ERR_INVALID, "bucket or hparams is NULL");
+  const int slots = slots_of(hp->kind);
+  if (slots < 0) return fail(OF_ERR_INVALID, "unknown optimizer kind %d", hp->kind);
+  if (flags & ~(OF_FLAG_DEVICE_STEP))
+    return fail(OF_ERR_INVALID, "flags 0x%x not supported by the peer step (gradients are always "
+                "zeroed; bf16 parameters follow from param_dtype)", flags);
+  if (!(hp->eta > 0.0)) return fail(OF_ERR_INVALID, "step size must be > 0, got %g", hp->eta);
+  if (flags & OF_FLAG_DEVICE_STEP) {
+    if (!hp->step_offset_dev || !hp->step_table_dev || hp->step_table_rows < 2)
+      return fail(OF_ERR_INVALID, "OF_FLAG_DEVICE_STEP needs step_offset_dev and a step table");
+  } else if ((hp->kind == OF_ADAM || hp->kind == OF_ADAMW) &&
+             (hp->bias_correction1 == 0.0 || hp->bias_correction2 == 0.0)) {
+    return fail(OF_ERR_INVALID, "adam bias corrections must be non-zero (step index t >= 1)");
+  }
+  if (b->world < 1 || b->world > OF_MAX_PEERS)
+    return fail(OF_ERR_INVALID, "world %d outside [1, %d]", b->world, OF_MAX_PEERS);
+  if (b->rank < 0 || b->rank >= b->world)
+    return fail(OF_ERR_INVALID, "rank %d outside [0, %d)", b->rank, b->world);
+  if (b->shard_begin < 0 || b->shard_len < 0 || (b->shard_begin % 4) || (b->shard_len % 4))
+    return fail(OF_ERR_INVALID, "shard [%lld, +%lld) must be non-negative multiples of 4",
+                (long long)b->shard_begin, (long long)b->shard_len);
+  if (!b->peer_grad || !b->peer_param) return fail(OF_ERR_INVALID, "peer pointer arrays are NULL");
+  PeerParams pp;
+  memset(&pp, 0, sizeof(pp));
+  for (int w = 0; w < b->world; ++w) {
+    if (!b->peer_grad[w] || !b->peer_param[w])
+      return fail(OF_ERR_INVALID, "peer %d has a NULL grad or param buffer", w);
+    pp.grad[w] = b->peer_grad[w];
+    pp.param[w] = b->peer_param[w];
+  }
+  const bool mixed = b->param_dtype == OF_BF16;
+  if (mixed && (b->grad_dtype != OF_BF16 || !b->master))
+    return fail(OF_ERR_INVALID, "bf16 parameters need bf16 gradients and an fp32 master shard");
+  if (!mixed && b->grad_dtype != b->param_dtype)
+    return fail(OF_ERR_UNSUPPORTED, "grad dtype %d with param dtype %d", b->grad_dtype, b->param_dtype);
+  if (slots >= 1 && !b->state0) return fail(OF_ERR_INVALID, "kind needs state0");
+  if (slots >= 2 && !b->state1) return fail(OF_ERR_INVALID, "kind needs state1");
+  pp.master = b->master;
+  pp.s0 = b->state0;
+  pp.s1 = b->state1;
+  pp.begin = b->shard_begin;
+  pp.len = b->shard_len;
+  pp.world = b->world;
+  pp.rank = b->rank;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (mixed) return dispatch_peer<float, __nv_bfloat16, true>(pp, hp, grad_scale_dev, flags, s);
+  if (b->param_dtype == OF_F32) return dispatch_peer<float, float, false>(pp, hp, grad_scale_dev, flags, s);
+  if (b->param_dtype == OF_F64) return dispatch_peer<double, double, false>(pp, hp, grad_scale_dev, flags, s);
+  return fail(OF_ERR_UNSUPPORTED, "param dtype %d", b->param_dtype);
 }
 
 }  // extern "C"

@@ -23,6 +23,14 @@ the remaining layers; the compute stream joins once at the end of backward.
 Forward fusion: the reduce-scatter happens in backward, the update +
 all-gather of each bucket are issued by its first layer's forward pre-hook,
 with the next bucket prefetched on the communication stream.
+
+``transport="peer"`` replaces the three steps by ONE kernel over NVLink peer
+memory (``of_dp_step_peer``): flat_param and flat_grad live in torch symmetric
+memory, so every rank can address every peer's buffers; the shard owner sums
+its shard of the gradients over the peers, updates it, writes the result into
+every peer's flat_param and zeroes the gradient shard it read, between two
+cross-rank barriers.  No staging buffer, no reduce-scatter output, and the
+all-gather traffic is issued by the same threads that computed the values.
 """
 
 from __future__ import annotations
@@ -36,11 +44,12 @@ from .engine import launch_groups
 from .errors import ConfigError, GlobalInfoRequired, StateError
 
 DEFAULT_BUCKET_ELEMS = 1 << 22  # 16 MiB of fp32 per bucket
+TRANSPORTS = ("nccl", "peer")
 
 
 class _Bucket:
     __slots__ = ("index", "params", "offsets", "flat_param", "flat_grad", "grad_shard", "slots",
-                 "shard", "master", "tl", "ready", "event", "done", "leader", "pending")
+                 "shard", "master", "tl", "peer", "hparam", "hgrad", "ready", "event", "done", "leader", "pending")
 
     def __init__(self, index):
         self.index = index
@@ -50,11 +59,16 @@ class DataParallelFusion:
     """Sharded fused optimizer of one Graph across a process group."""
 
     def __init__(self, graph, policy, *, group=None, bucket_elems: int = DEFAULT_BUCKET_ELEMS,
-                 update_fn=None):
+                 update_fn=None, transport: str = "nccl"):
         if not dist.is_initialized():
             raise StateError("torch.distributed is not initialised")
         if policy.kind == "newton":
             raise ConfigError("newton has no per-parameter step")
+        if transport not in TRANSPORTS:
+            raise ConfigError(f"transport must be one of {TRANSPORTS}, got {transport!r}")
+        if transport == "peer" and (update_fn is not None or graph.device.type != "cuda"):
+            raise ConfigError("the peer transport runs the fused CUDA kernel over symmetric memory")
+        self.transport = transport
         self.graph = graph
         self.policy = policy
         self.group = group
@@ -68,6 +82,7 @@ class DataParallelFusion:
         elif update_fn is None:
             raise ConfigError("the sharded update runs on CUDA; pass update_fn only for host tests")
         self.comm = torch.cuda.Stream() if self.cuda else None
+        self._sync = None
         slots = policy.history_slots()
         # mixed precision (C4): the module runs in bf16 with fp32 masters
         # (Graph.use_master_weights).  Gradients are reduce-scattered in bf16;
@@ -99,8 +114,12 @@ class DataParallelFusion:
                 n += -(-p.value.numel() // align) * align
             padded = -(-n // unit) * unit
             S = padded // self.world
-            b.flat_param = torch.zeros(padded, dtype=dt, device=self.device)
-            b.flat_grad = torch.zeros(padded, dtype=dt, device=self.device)
+            if transport == "peer":   # symmetric buffers, mapped into every peer
+                b.flat_param, b.hparam = self._symmetric(padded, dt)
+                b.flat_grad, b.hgrad = self._symmetric(padded, dt)
+            else:
+                b.flat_param = torch.zeros(padded, dtype=dt, device=self.device)
+                b.flat_grad = torch.zeros(padded, dtype=dt, device=self.device)
             flat_master = torch.zeros(padded, dtype=mdt, device=self.device) if self.mixed else None
             with torch.no_grad():
                 for p, off in zip(b.params, b.offsets):
@@ -120,7 +139,9 @@ class DataParallelFusion:
             else:
                 dist.broadcast(b.flat_param, src=src, group=group)
             b.shard = slice(self.rank * S, (self.rank + 1) * S)
-            b.grad_shard = torch.zeros(S, dtype=dt, device=self.device)
+            # (the peer transport reads the shard straight from every peer's
+            # flat_grad: no reduce-scatter destination)
+            b.grad_shard = torch.zeros(S if transport == "nccl" else 0, dtype=dt, device=self.device)
             b.slots = {name: torch.zeros(S, dtype=mdt, device=self.device) for name in slots}
             # the owned fp32 master shard (state memory / W); the full-size
             # per-parameter masters are released: a non-DP schedule on this
@@ -138,6 +159,11 @@ class DataParallelFusion:
                            b.slots[slots[1]] if len(slots) > 1 else None)
                 tl.set_dtypes(mdt, dt)
                 b.tl = tl
+                if transport == "peer":
+                    sl = [b.slots[k] for k in slots] + [None, None]
+                    b.peer = kernels.PeerBucket(
+                        self.world, self.rank, dt, dt, b.hgrad.buffer_ptrs, b.hparam.buffer_ptrs,
+                        b.master, sl[0], sl[1], b.shard.start, S)
                 b.event = torch.cuda.Event()
                 b.done = torch.cuda.Event()
             b.ready = 0
@@ -155,13 +181,47 @@ class DataParallelFusion:
         self._leader_handles = None
         self.join_event = torch.cuda.Event() if self.cuda else None
 
+    def _symmetric(self, n: int, dt):
+        """A zeroed flat buffer in torch symmetric memory and its handle (the
+        peers' mappings of it: ``buffer_ptrs``; cross-rank ``barrier``)."""
+        import torch.distributed._symmetric_memory as symm_mem
+        t = symm_mem.empty(n, dtype=dt, device=self.device)
+        t.zero_()
+        grp = self.group if self.group is not None else dist.group.WORLD
+        h = symm_mem.rendezvous(t, grp)
+        if self._sync is None:
+            self._sync = h
+        return t, h
+
     # -- the per-bucket pipeline ----------------------------------------------
 
     def _reduce_scatter(self, b) -> None:
+        if self.transport == "peer":
+            return   # the fused kernel reads every peer's gradients in place
         dist.reduce_scatter_tensor(b.grad_shard, b.flat_grad, op=dist.ReduceOp.SUM, group=self.group)
         b.flat_grad.zero_()
 
     def _update_and_gather(self, b, t: int) -> None:
+        if self.transport == "peer":
+            # barrier: every rank's gradients of this bucket are complete; one
+            # kernel sums the shard over the peers, updates it and writes it
+            # to every peer; barrier: those writes (and the gradient zeroing)
+            # landed before any rank reads parameters or accumulates again
+            # All of them go on the communication stream, whatever stream the
+            # caller is on: the barriers of one rank then run in host issue
+            # order, which is the same on every rank.
+            cur = torch.cuda.current_stream()
+            on_comm = cur == self.comm
+            if not on_comm:
+                self.comm.wait_stream(cur)
+            with torch.cuda.stream(self.comm):
+                self._sync.barrier(channel=0)
+                kernels.dp_step_peer(b.peer, self.policy._hparams(t), self.scale,
+                                     self.policy.device_step_flag, None)
+                self._sync.barrier(channel=0)
+            if not on_comm:
+                cur.wait_stream(self.comm)
+            return
         if self.update_fn is not None:
             if self.mixed:    # host stand-in: fp32 grad shard, master updated, bf16 written back
                 g = b.grad_shard.float().mul_(1.0 / self.world)

@@ -95,6 +95,34 @@ def policy_step(tl: TensorList, hp: nat.OfHparams, grad_scale, flags: int, strea
         nat.check(st, "of_policy_step_mt")
 
 
+class PeerBucket:
+    """Host ``of_peer_bucket`` of one data-parallel bucket (pointers fixed at
+    construction: the symmetric buffers never move)."""
+
+    __slots__ = ("grads", "params", "struct", "ref")
+
+    def __init__(self, world: int, rank: int, param_dtype, grad_dtype, peer_grad_ptrs,
+                 peer_param_ptrs, master, state0, state1, shard_begin: int, shard_len: int):
+        self.grads = (ctypes.c_void_p * world)(*peer_grad_ptrs)
+        self.params = (ctypes.c_void_p * world)(*peer_param_ptrs)
+        pp = nat._PP
+
+        def ptr(t):
+            return t.data_ptr() if t is not None else None
+        self.struct = nat.OfPeerBucket(world, rank, dtype_code(param_dtype), dtype_code(grad_dtype),
+                                       ctypes.cast(self.grads, pp), ctypes.cast(self.params, pp),
+                                       ptr(master), ptr(state0), ptr(state1), shard_begin, shard_len)
+        self.ref = ctypes.byref(self.struct)
+
+
+def dp_step_peer(pb: PeerBucket, hp: nat.OfHparams, grad_scale, flags: int, stream) -> None:
+    """of_dp_step_peer: reduce-scatter + update + all-gather of one bucket in one kernel."""
+    gs = grad_scale.data_ptr() if grad_scale is not None else None
+    st = nat.lib().of_dp_step_peer(pb.ref, ctypes.byref(hp), gs, flags, _handle(stream))
+    if st:
+        nat.check(st, "of_dp_step_peer")
+
+
 def sqnorm(tl: TensorList, workspace: torch.Tensor, out: torch.Tensor, accumulate: bool,
            stream) -> None:
     st = nat.lib().of_sqnorm_mt(tl.ref, workspace.data_ptr(), workspace.numel(), out.data_ptr(),

@@ -3,6 +3,8 @@ declares; argument validation rejects bad calls before anything is launched
 (no GPU needed: nothing here reaches the CUDA runtime)."""
 
 import ctypes
+
+import torch
 import re
 from pathlib import Path
 
@@ -77,6 +79,26 @@ def test_invalid_arguments_rejected_before_launch():
     assert so.of_policy_step_mt(tl.ref, ctypes.byref(adam), None, dev, None) == nat.OF_ERR_INVALID
     assert b"rows" in so.of_last_error()
     assert so.of_step_advance(None, 1, None) == nat.OF_ERR_INVALID
+    # the data-parallel peer step validates world/rank/shard/pointers first
+    pb = kernels.PeerBucket(2, 0, torch.float32, torch.float32, [0x1000, 0x2000], [0x3000, 0x4000],
+                            None, None, None, 0, 8)
+    sgdm = _hp()
+    assert so.of_dp_step_peer(pb.ref, ctypes.byref(sgdm), None, 0, None) == nat.OF_ERR_INVALID
+    assert b"state0" in so.of_last_error()
+    pb.struct.state0 = 0x5000
+    pb.struct.rank = 2
+    assert so.of_dp_step_peer(pb.ref, ctypes.byref(sgdm), None, 0, None) == nat.OF_ERR_INVALID
+    pb.struct.rank = 0
+    pb.struct.shard_len = 6
+    assert so.of_dp_step_peer(pb.ref, ctypes.byref(sgdm), None, 0, None) == nat.OF_ERR_INVALID
+    pb.struct.shard_len = 8
+    pb.struct.world = nat.OF_MAX_PEERS + 1
+    assert so.of_dp_step_peer(pb.ref, ctypes.byref(sgdm), None, 0, None) == nat.OF_ERR_INVALID
+    pb.struct.world = 2
+    pb.struct.param_dtype = nat.OF_BF16      # bf16 params need bf16 grads and a master
+    assert so.of_dp_step_peer(pb.ref, ctypes.byref(sgdm), None, 0, None) == nat.OF_ERR_INVALID
+    assert so.of_dp_step_peer(pb.ref, ctypes.byref(sgdm), None, nat.OF_FLAG_ZERO_GRAD,
+                              None) == nat.OF_ERR_INVALID
     empty = kernels.TensorList(0)
     assert so.of_policy_step_mt(empty.ref, ctypes.byref(hp), None, 0, None) == nat.OF_OK
     assert so.of_clip_coef(None, 1.0, None, None, None) == nat.OF_ERR_INVALID

@@ -30,3 +30,11 @@ if [ -n "${NCU_MIXED}" ]; then
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:mt_step -s 1 -c 1 \
     -o gpurun_out/prof_r50mixed -f python tools/profile_kernels.py r50mixed > gpurun_out/ncu_r50mixed.log 2>&1; echo ncu_r50mixed=$?
 fi
+# raw-page CSV exports (small) instead of the .ncu-rep files (gpurun_out/ must stay < 64 MiB)
+for r in gpurun_out/prof_*.ncu-rep; do
+  [ -f "$r" ] || continue
+  ncu -i "$r" --page raw --csv > "${r%.ncu-rep}.raw.csv" 2>/dev/null
+  ncu -i "$r" --page details --csv > "${r%.ncu-rep}.details.csv" 2>/dev/null
+  [ -n "${KEEP_REPS}" ] || rm -f "$r"
+done
+ls -la gpurun_out | tail -20

@@ -48,10 +48,17 @@ def launches(path):
             print(f"| `{n}` | {g} | {v / 1e3:.2f} |")
 
 
-def report(path, title):
+def _raw_rows(path):
+    """Rows of ncu's raw page: from a .ncu-rep (needs ncu) or its CSV export."""
+    if path.endswith(".csv"):
+        return list(csv.reader(open(path)))
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
-    rows = list(csv.reader(io.StringIO(out)))
+    return list(csv.reader(io.StringIO(out)))
+
+
+def report(path, title):
+    rows = _raw_rows(path)
     hdr, units = rows[0], rows[1]
     print(f"# {title}\n\nSource: `{path}` (`ncu --set full --clock-control none`)\n")
     idx = [(m, hdr.index(m)) for m in METRICS if m in hdr]
@@ -68,9 +75,7 @@ def traffic(path, key, out_json):
     merged into ``out_json`` under ``key`` (read by bench.py's roofline)."""
     import json
     import os
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
-                         text=True, check=True).stdout
-    rows = list(csv.reader(io.StringIO(out)))
+    rows = _raw_rows(path)
     hdr, units = rows[0], rows[1]
 
     def val(r, m):
