@@ -182,7 +182,10 @@ def timed(step, steps: int, warmup: int, dist: Dist, flush=None) -> float:
     dist.barrier()
     s = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.nvtx.range_push("timed")   # ncu --nvtx --nvtx-include timed/ selects this region
+    # a start/end range is process-wide (push/pop ranges are per thread and would
+    # miss the backward kernels autograd launches from its own thread):
+    # ncu --nvtx --nvtx-include timed selects this region
+    rng = torch.cuda.nvtx.range_start("timed")
     e0.record(s)
     for _ in range(steps):
         if flush is not None:
@@ -190,7 +193,7 @@ def timed(step, steps: int, warmup: int, dist: Dist, flush=None) -> float:
         step()
     e1.record(s)
     torch.cuda.synchronize()
-    torch.cuda.nvtx.range_pop()
+    torch.cuda.nvtx.range_end(rng)
     dist.barrier()
     return dist.max(e0.elapsed_time(e1)) / steps
 

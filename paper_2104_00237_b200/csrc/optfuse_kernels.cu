@@ -34,7 +34,22 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kVec = 4;
-constexpr int kUnroll = 4;
+#ifndef OF_UNROLL
+#define OF_UNROLL 4
+#endif
+#ifndef OF_MIN_BLOCKS
+#define OF_MIN_BLOCKS 1
+#endif
+#ifndef OF_UNROLL_BF16
+#define OF_UNROLL_BF16 2
+#endif
+#ifndef OF_MIN_BLOCKS_BF16
+#define OF_MIN_BLOCKS_BF16 4
+#endif
+#ifndef OF_CS
+#define OF_CS 0
+#endif
+constexpr int kUnroll = OF_UNROLL;
 constexpr int kTile = kThreads * kVec * kUnroll;  // elements per tile
 constexpr int kCtasPerSm = 8;
 constexpr int kCapMax = 256;                      // tensors per launch (param block)
@@ -293,6 +308,36 @@ __device__ __forceinline__ void st4_zero(double* p) {
 }
 __device__ __forceinline__ void st4_zero(__nv_bfloat16* p) { *reinterpret_cast<uint2*>(p) = make_uint2(0u, 0u); }
 
+// Read-once streams (gradient, history) with the evict-first hint when
+// OF_CS=1: they are not reused by anything that follows the update.
+#if OF_CS
+__device__ __forceinline__ void ld4s(const float* p, float (&v)[4]) {
+  const float4 t = __ldcs(reinterpret_cast<const float4*>(p));
+  v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+}
+__device__ __forceinline__ void ld4s(const double* p, double (&v)[4]) {
+  const double2 a = __ldcs(reinterpret_cast<const double2*>(p));
+  const double2 b = __ldcs(reinterpret_cast<const double2*>(p) + 1);
+  v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+}
+__device__ __forceinline__ void ld4s(const __nv_bfloat16* p, float (&v)[4]) {
+  const uint2 t = __ldcs(reinterpret_cast<const uint2*>(p));
+  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&t.x));
+  const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&t.y));
+  v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+}
+__device__ __forceinline__ void st4s(float* p, const float (&v)[4]) {
+  __stcs(reinterpret_cast<float4*>(p), make_float4(v[0], v[1], v[2], v[3]));
+}
+__device__ __forceinline__ void st4s(double* p, const double (&v)[4]) {
+  __stcs(reinterpret_cast<double2*>(p), make_double2(v[0], v[1]));
+  __stcs(reinterpret_cast<double2*>(p) + 1, make_double2(v[2], v[3]));
+}
+#else
+template <class P, class V> __device__ __forceinline__ void ld4s(const P* p, V (&v)[4]) { ld4(p, v); }
+template <class P, class V> __device__ __forceinline__ void st4s(P* p, const V (&v)[4]) { st4(p, v); }
+#endif
+
 template <class T> __device__ __forceinline__ T ld1(const T* p) { return *p; }
 __device__ __forceinline__ float ld1(const __nv_bfloat16* p) { return __bfloat162float(*p); }
 template <class G> __device__ __forceinline__ void st1_zero(G* p) { *p = G(0); }
@@ -305,11 +350,26 @@ __device__ __forceinline__ bool aligned(const void* p, unsigned a) {
   return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0;
 }
 
+// Per gradient type: vectors per thread per tile and the CTAs per SM the
+// register budget must allow.  fp32/f64 gradients: 4 vectors in flight per
+// thread at 2 CTAs/SM (measured best for VGG-16 / BERT); bf16 gradients (fp32
+// master + bf16 shadow, 8 streams per element): 2 vectors at 4 CTAs/SM -- the
+// 4-vector build needs 108 registers and stalls at 16 warps/SM (ncu: 52% of
+// DRAM peak on ResNet-50), the 2-vector one reaches 0.80 of the copy peak.
+template <class G> struct Tune {
+  static constexpr int kUnr = OF_UNROLL;
+  static constexpr int kMinBlocks = OF_MIN_BLOCKS;
+};
+template <> struct Tune<__nv_bfloat16> {
+  static constexpr int kUnr = OF_UNROLL_BF16;
+  static constexpr int kMinBlocks = OF_MIN_BLOCKS_BF16;
+};
+
 // One multi-tensor policy step.  T: param/state type; G: grad type; UNR:
 // vectors per thread per tile (tile = 256 * 4 * UNR elements).  Small lists
 // use UNR=1 so that even a few MB spread over more CTAs than there are SMs.
 template <class Op, class T, class G, int CAP, int UNR>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, Tune<G>::kMinBlocks)
 mt_step_kernel(const __grid_constant__ MTParams<CAP> mp, const Op op_in,
                const float* __restrict__ gscale, uint32_t flags, const StepSrc step) {
   using GV = typename GradVal<G>::type;
@@ -354,9 +414,9 @@ mt_step_kernel(const __grid_constant__ MTParams<CAP> mp, const Op op_in,
           const int j = threadIdx.x + (r + u) * kThreads;
           if (j < nvec) {
             ld4(p + 4 * j, vp[u]);
-            ld4(g + 4 * j, vg[u]);
-            if (Op::kSlots >= 1) ld4(s0 + 4 * j, v0[u]);
-            if (Op::kSlots >= 2) ld4(s1 + 4 * j, v1[u]);
+            ld4s(g + 4 * j, vg[u]);
+            if (Op::kSlots >= 1) ld4s(s0 + 4 * j, v0[u]);
+            if (Op::kSlots >= 2) ld4s(s1 + 4 * j, v1[u]);
           }
         }
 #pragma unroll
@@ -370,8 +430,8 @@ mt_step_kernel(const __grid_constant__ MTParams<CAP> mp, const Op op_in,
               op(vp[u][k], gk, v0[u][k], v1[u][k]);
             }
             st4(p + 4 * j, vp[u]);
-            if (Op::kSlots >= 1) st4(s0 + 4 * j, v0[u]);
-            if (Op::kSlots >= 2) st4(s1 + 4 * j, v1[u]);
+            if (Op::kSlots >= 1) st4s(s0 + 4 * j, v0[u]);
+            if (Op::kSlots >= 2) st4s(s1 + 4 * j, v1[u]);
             if (zero_grad) st4_zero(g + 4 * j);
             if (shadow) st4_bf16(sh + 4 * j, vp[u]);
           }
@@ -516,8 +576,9 @@ template <class Op, class T, class G, int CAP>
 int launch_step_chunk(const of_tensor_list* l, int first, int count, const Op& op,
                       const float* gscale, uint32_t flags, const StepSrc& step, int max_ctas,
                       cudaStream_t s) {
+  constexpr int U = Tune<G>::kUnr;
   MTParams<CAP> mp;
-  int64_t tiles = pack<CAP>(l, first, count, mp, kTile);
+  int64_t tiles = pack<CAP>(l, first, count, mp, kThreads * kVec * U);
   if (tiles == 0) return OF_OK;
   int64_t cap = static_cast<int64_t>(sm_count()) * kCtasPerSm;
   if (max_ctas > 0 && max_ctas < cap) cap = max_ctas;
@@ -530,7 +591,7 @@ int launch_step_chunk(const of_tensor_list* l, int first, int count, const Op& o
   }
   if (tiles > INT32_MAX) return fail(OF_ERR_INVALID, "tensor list too large for one launch");
   const int grid = static_cast<int>(tiles < cap ? tiles : cap);
-  mt_step_kernel<Op, T, G, CAP, kUnroll><<<grid, kThreads, 0, s>>>(mp, op, gscale, flags, step);
+  mt_step_kernel<Op, T, G, CAP, U><<<grid, kThreads, 0, s>>>(mp, op, gscale, flags, step);
   return check_launch("mt_step_kernel");
 }
 

@@ -13,11 +13,11 @@ tail -c 400 gpurun_out/bench.log
 fi
 if [ -n "${NCU}" ]; then
   # launch list of the headline command (NVTX-selected timed region)
-  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --replay-mode application --nvtx --nvtx-include "timed/" -c 3000 --csv \
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --replay-mode application --nvtx --nvtx-include "timed" -c 3000 --csv \
     --log-file gpurun_out/launches.csv python bench.py --no-extras --steps 4 --warmup 3 --instances 1 > gpurun_out/ncu_bench.log 2>&1; echo ncu_list=$?
   # the same step eager (no CUDA graph): cuDNN's semi-persistent batch-norm kernel fails to
   # launch under the profiler when it is a graph node
-  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "timed/" -c 3000 --csv \
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "timed" -c 3000 --csv \
     --log-file gpurun_out/launches_eager.csv python bench.py --no-extras --graphs 0 --steps 4 --warmup 3 --instances 1 > gpurun_out/ncu_bench_eager.log 2>&1; echo ncu_list_eager=$?
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:mt_step -s 40 -c 8 \
     -o gpurun_out/prof_bf -f python tools/profile_kernels.py bf > gpurun_out/ncu_bf.log 2>&1; echo ncu_bf=$?
