@@ -329,9 +329,11 @@ def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
                 return of.run_baseline(g, pol, inp, timing=False).loss
         elif schedule == "forward-fusion":
             fbe = args.ff_bucket_elems if bucket_elems is None else bucket_elems
+            pre = workers == 2   # forward fusion: an explicit workers=2 selects the side-stream lookahead
 
             def run(inp):
-                return of.run_forward_fusion(g, pol, inp, timing=False, bucket_elems=fbe).loss
+                return of.run_forward_fusion(g, pol, inp, timing=False, bucket_elems=fbe,
+                                             prefetch=pre).loss
         else:
             be = args.bucket_elems if bucket_elems is None else bucket_elems
 
@@ -355,7 +357,7 @@ def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
 def measure_update_kernel(args, device, peaks) -> dict:
     """Standalone roofline of the multi-tensor kernel: one pass over a whole
     parameter set (as few launches as the 256-tensor parameter block allows),
-    L2 flushed before every pass: VGG-16 with Adam (C3, update-bound),
+    L2 flushed (and its dirty lines written back) before every pass: VGG-16 with Adam (C3, update-bound),
     BERT-base with AdamW (C5), ResNet-50 bf16 + fp32 masters with AdamW (C4:
     bf16 grad in, bf16 parameter out) and MobileNetV2 with SGD-momentum (C2)."""
     import torch
@@ -380,7 +382,8 @@ def measure_update_kernel(args, device, peaks) -> dict:
         times = []
         for i in range(8):
             pol.begin_iteration()
-            flush.zero_()
+            flush.zero_()                  # evict the parameter set from L2 ...
+            flush.sum()                    # ... and write the flush's dirty lines back now
             torch.cuda._sleep(4_000_000)   # the host builds the tensor list while the GPU waits
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
@@ -510,7 +513,9 @@ def _variants_c2(world: int):
          ("cl:graph:ours:backward-fusion(w=2,bucket=1M)", "backward-fusion", 2, None, None, 4 * K, True, True),
          ("cl:graph:ours:backward-fusion(w=2,bucket=4M)", "backward-fusion", 2, None, None, 16 * K, True, True),
          ("cl:graph:ours:backward-fusion(w=1,bucket=256K)", "backward-fusion", 1, None, None, K, True, True),
-         ("cl:graph:ours:forward-fusion(bucket=1M)", "forward-fusion", None, None, None, 4 * K, True, True)]
+         ("cl:graph:ours:forward-fusion(bucket=1M)", "forward-fusion", None, None, None, 4 * K, True, True),
+         ("cl:graph:ours:forward-fusion(bucket=256K,prefetch)", "forward-fusion", 2, None, None, K, True, True),
+         ("ours:forward-fusion(bucket=256K,prefetch)", "forward-fusion", 2, None, None, K, False, False)]
     if world > 1:
         v = [x for x in v if not x[6]]
     return v
@@ -639,7 +644,13 @@ def run_ours(args) -> dict:
             if wl in args.extras.split(","):
                 res[key] = run_extra(args, wl, device, dist, flush)
         res["e2e"] = e2e(args, device, dist)
-        ins = measure_in_situ(args, device, peaks, 5)
+        # the kernel's own duration is a per-GPU quantity: measured on this
+        # GPU's single-process engine whatever the world size
+        world, args.world = args.world, 1
+        try:
+            ins = measure_in_situ(args, device, peaks, 5)
+        finally:
+            args.world = world
         std = measure_update_kernel(args, device, peaks)
         tr = ncu_traffic("c2_backward_fusion_buckets")
         res["roofline"] = {"bound": "hbm", "kernel": "mt_step_kernel (backward-fusion, side stream)",
@@ -678,6 +689,7 @@ def _variants_extra(wl: str):
         v.append(("ours:backward-fusion(w=2,per-layer,capped)", "backward-fusion", -1, None, 0, False))
     else:
         v.append(("ours:forward-fusion(bucket=1M)", "forward-fusion", None, None, 1 << 20, False))
+        v.append(("ours:forward-fusion(bucket=1M,prefetch)", "forward-fusion", 2, None, 1 << 20, False))
         v.append(("ours:backward-fusion(w=2,bucket=1M)", "backward-fusion", 2, None, 1 << 20, False))
     # the same iteration captured as one CUDA graph (Adam/AdamW replay through
     # the device-side step index; torch's Adam with capturable=True)
@@ -686,6 +698,7 @@ def _variants_extra(wl: str):
           ("graph:" + LB, "baseline", None, "none", 0, True),
           ("graph:ours:baseline", "baseline", None, None, 0, True),
           ("graph:ours:forward-fusion(bucket=1M)", "forward-fusion", None, None, 1 << 20, True),
+          ("graph:ours:forward-fusion(bucket=1M,prefetch)", "forward-fusion", 2, None, 1 << 20, True),
           ("graph:ours:backward-fusion(w=2,bucket=1M)", "backward-fusion", 2, None, 1 << 20, True)]
     if WORKLOADS[wl].get("mixed"):
         v.append(("graph:" + OWN_LB, "baseline", None, "none-mixed", 0, True))

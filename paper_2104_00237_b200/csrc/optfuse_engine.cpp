@@ -123,6 +123,9 @@ class Engine : public std::enable_shared_from_this<Engine> {
     for (auto& G : groups_)
       if (G.ready) cudaEventDestroy(G.ready);
     if (join_) cudaEventDestroy(join_);
+    for (auto e : prefetch_done_)
+      if (e) cudaEventDestroy(e);
+    if (prefetch_group_.ready) cudaEventDestroy(prefetch_group_.ready);
     clear_profile();
   }
 
@@ -278,6 +281,50 @@ class Engine : public std::enable_shared_from_this<Engine> {
     return static_cast<int>(scratch_.members.size());
   }
 
+  // Forward fusion with one-unit lookahead (needs the side stream): the
+  // update of unit u+1 is issued on the side stream when unit u's pre-hook
+  // runs, so it overlaps unit u's forward instead of sitting on the compute
+  // stream's critical path; unit u+1's pre-hook makes the compute stream wait
+  // for it.  Nothing reads unit u+1's parameters in between (a parameter
+  // belongs to the unit of the first layer that uses it, and the latch skips
+  // parameters already updated), the previous backward is ordered before the
+  // prefetch by an event, and the released gradients are held until the
+  // compute stream has waited, so the allocator cannot hand them to the
+  // forward while the side stream still reads them.
+  int ff_unit_lookahead(int u) {
+    if (!side_) return ff_layer(u);
+    const int nu = static_cast<int>(ff_units_.size());
+    if (prefetch_done_.size() != static_cast<size_t>(nu)) {
+      for (auto e : prefetch_done_)
+        if (e) cudaEventDestroy(e);
+      prefetch_done_.assign(nu, nullptr);
+      prefetch_hold_.assign(nu, {});
+      prefetched_.assign(nu, 0);
+    }
+    cudaStream_t cur = current();
+    int n = 0;
+    if (prefetched_.at(u)) {
+      cuda_check(cudaStreamWaitEvent(cur, prefetch_done_[u], 0), "cudaStreamWaitEvent");
+      prefetch_hold_[u].clear();
+      prefetched_[u] = 0;
+    } else {
+      n = ff_layer(u);
+    }
+    if (u + 1 < nu) n += prefetch_unit(u + 1, cur);
+    return n;
+  }
+
+  // Joins every prefetched unit whose layer did not run this forward.
+  void ff_join() {
+    cudaStream_t cur = current();
+    for (size_t u = 0; u < prefetched_.size(); ++u) {
+      if (!prefetched_[u]) continue;
+      cuda_check(cudaStreamWaitEvent(cur, prefetch_done_[u], 0), "cudaStreamWaitEvent");
+      prefetch_hold_[u].clear();
+      prefetched_[u] = 0;
+    }
+  }
+
   // Updates every pending parameter (layer order, each once) on the current
   // stream: forward-fusion leftovers and flush_pending_updates.
   int flush() {
@@ -391,6 +438,37 @@ class Engine : public std::enable_shared_from_this<Engine> {
     launched_[gi] = 1;
   }
 
+  int prefetch_unit(int u, cudaStream_t cur) {
+    Group& G = prefetch_group_;
+    G.members.clear();
+    for (int idx : ff_units_[u])
+      if (pending_[idx] && !updated_[idx]) G.members.push_back(idx);
+    if (G.members.empty()) return 0;
+    G.bind();
+    G.elems = 0;
+    for (int idx : G.members) G.elems += params_[idx].numel();
+    refresh_static(G);
+    const size_t held = hold_.size();
+    fill_grads(G);                       // (zero gradients, if any, on the compute stream)
+    if (!G.ready) cuda_check(cudaEventCreateWithFlags(&G.ready, cudaEventDisableTiming), "cudaEventCreate");
+    cuda_check(cudaEventRecord(G.ready, cur), "cudaEventRecord");
+    cuda_check(cudaStreamWaitEvent(side_, G.ready, 0), "cudaStreamWaitEvent");
+    launch(G, side_);
+    release(G);
+    if (!prefetch_done_[u])
+      cuda_check(cudaEventCreateWithFlags(&prefetch_done_[u], cudaEventDisableTiming), "cudaEventCreate");
+    cuda_check(cudaEventRecord(prefetch_done_[u], side_), "cudaEventRecord");
+    // gradients this launch reads stay referenced until the compute stream waited
+    prefetch_hold_[u].assign(hold_.begin() + held, hold_.end());
+    hold_.resize(held);
+    prefetched_[u] = 1;
+    for (int idx : G.members) {
+      updated_[idx] = 1;
+      pending_[idx] = 0;
+    }
+    return static_cast<int>(G.members.size());
+  }
+
   void launch_dynamic(Group& G, cudaStream_t s) {
     G.bind();
     G.elems = 0;
@@ -414,7 +492,10 @@ class Engine : public std::enable_shared_from_this<Engine> {
   std::vector<std::vector<int>> layers_;
   std::vector<std::vector<int>> ff_units_;
   std::vector<Group> groups_;
-  Group scratch_;
+  Group scratch_, prefetch_group_;
+  std::vector<cudaEvent_t> prefetch_done_;
+  std::vector<std::vector<at::Tensor>> prefetch_hold_;
+  std::vector<uint8_t> prefetched_;
   std::vector<int> group_of_, ready_;
   std::vector<uint8_t> launched_, pending_, updated_;
   std::vector<at::Tensor> hold_;
@@ -462,6 +543,8 @@ PYBIND11_MODULE(_optfuse_engine, m) {
       .def("set_updated", &Engine::set_updated)
       .def("num_pending", &Engine::num_pending)
       .def("ff_layer", &Engine::ff_layer)
+      .def("ff_unit_lookahead", &Engine::ff_unit_lookahead)
+      .def("ff_join", &Engine::ff_join)
       .def("set_ff_units", &Engine::set_ff_units)
       .def("reset_ff_units", &Engine::reset_ff_units)
       .def("flush", &Engine::flush)

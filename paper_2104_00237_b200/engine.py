@@ -90,6 +90,7 @@ class FusionEngine:
             self.native.set_slots(p.id, a, b, p.master)
         self._hp_key = None
         self.ff_bucket_elems = 0
+        self.ff_prefetch = False
         self.ff_leaders = None
 
     def configure(self, policy, step_t: int, grad_scale=None, max_ctas: int = 0) -> None:

@@ -291,3 +291,66 @@ def test_capped_grid_same_bits(max_ctas):
     for p, (th, g) in zip(ps, ref):
         optim_ref.step("adam", h, th, g, {}, 1)
         assert p.cpu().numpy().tobytes() == th.tobytes()
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+@pytest.mark.parametrize("kind", ["sgd-momentum", "adam"])
+@pytest.mark.parametrize("mixed", [False, True])
+def test_peer_step_simulated_ranks_on_one_gpu(world, kind, mixed):
+    """of_dp_step_peer with W "ranks" whose buffers all live on this GPU (plain
+    device pointers stand in for the NVLink peer mappings): the multi-peer
+    logic -- rank-order gradient sum, 1/W scale, the update of each owned
+    shard, parameter writes into every peer, gradient zeroing in every peer --
+    against the oracle on the averaged gradient, bit for bit (fp32, and bf16
+    parameters with fp32 master shards)."""
+    rng = np.random.default_rng(5)
+    n = 4 * world * 37
+    S = n // world
+    eta, wd = ETA[kind], 1e-3
+    theta0 = rng.standard_normal(n).astype(np.float32)
+    grads = [rng.standard_normal(n).astype(np.float32) for _ in range(world)]
+    if mixed:   # bf16 model: parameters and gradients are bf16, masters fp32
+        grads = [torch.from_numpy(g).to(torch.bfloat16).float().numpy() for g in grads]
+        params = [torch.from_numpy(theta0).to(DEV).to(torch.bfloat16) for _ in range(world)]
+        gbufs = [torch.from_numpy(g).to(DEV).to(torch.bfloat16) for g in grads]
+        masters = [torch.from_numpy(theta0[r * S:(r + 1) * S].copy()).to(DEV) for r in range(world)]
+    else:
+        params = [torch.from_numpy(theta0.copy()).to(DEV) for _ in range(world)]
+        gbufs = [torch.from_numpy(g.copy()).to(DEV) for g in grads]
+        masters = [None] * world
+    names = optim_ref.SLOTS[kind]
+    states = [[torch.zeros(S, device=DEV) for _ in names] + [None, None] for _ in range(world)]
+    scale = torch.full((), 1.0 / world, dtype=torch.float32, device=DEV)
+    pdt = torch.bfloat16 if mixed else torch.float32
+    for t in (1, 2):
+        hp = kernels.hparams(kind, eta, 0.9, wd, 1e-8, 0.9, 0.999, 0.9, t)
+        if t == 2:   # fresh gradients for the second step
+            for w in range(world):
+                gbufs[w].copy_(torch.from_numpy(grads[w]).to(gbufs[w].dtype))
+        for r in range(world):
+            pb = kernels.PeerBucket(world, r, pdt, pdt, [g.data_ptr() for g in gbufs],
+                                    [p.data_ptr() for p in params], masters[r], states[r][0],
+                                    states[r][1], r * S, S)
+            kernels.dp_step_peer(pb, hp, scale, 0, None)
+    torch.cuda.synchronize()
+    theta = theta0.copy()
+    slots = {}
+    h = optim_ref.Hyper(kind=kind, eta=eta, weight_decay=wd)
+    for t in (1, 2):
+        g = grads[0].copy()
+        for w in range(1, world):
+            g = np.add(g, grads[w])
+        g = np.multiply(g, np.float32(1.0 / world))
+        optim_ref.step(kind, h, theta, g, slots, t)
+    for r in range(world):
+        assert not gbufs[r].float().any(), f"rank {r}: gradient not zeroed"
+        if mixed:
+            want = torch.from_numpy(theta).to(torch.bfloat16)
+            assert torch.equal(params[r].cpu(), want), f"rank {r}: bf16 parameters"
+            got_m = masters[r].cpu().numpy()
+            assert got_m.tobytes() == theta[r * S:(r + 1) * S].tobytes()
+        else:
+            assert params[r].cpu().numpy().tobytes() == theta.tobytes(), f"rank {r}: parameters"
+        for k, name in enumerate(names):
+            got = states[r][k].cpu().numpy()
+            assert got.tobytes() == slots[name][r * S:(r + 1) * S].tobytes(), (r, name)

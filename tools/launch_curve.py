@@ -42,6 +42,7 @@ def main():
             ts = []
             for _ in range(3):
                 flush.zero_()
+                flush.sum()
                 torch.cuda._sleep(200_000_000)   # ~0.1 s: the host enqueues the whole sequence first
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
