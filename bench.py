@@ -67,6 +67,9 @@ def parse_args(argv=None):
                     help="1: capture each iteration (ours and the torch baseline) as a CUDA graph")
     ap.add_argument("--channels-last", type=int, default=1, help="1: NHWC model and inputs")
     ap.add_argument("--no-extras", action="store_true", help="headline only (for profilers)")
+    ap.add_argument("--force-dp", action="store_true",
+                    help="run the data-parallel code path (NCCL process group, DataParallelFusion, "
+                         "DDP baselines) even at one GPU: the N>1 path's smoke test")
     ap.add_argument("--extras", default="c1,c3,c4,c5",
                     help="other BASELINE.json configs timed beside the headline ('' to skip)")
     ap.add_argument("--cpu-iters", type=int, default=2, help="CPU baseline sample iterations")
@@ -86,10 +89,10 @@ class Dist:
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
 
-    def init(self, backend="nccl"):
+    def init(self, backend="nccl", force: bool = False):
         import torch
         import torch.distributed as dist
-        if self.world > 1:
+        if self.world > 1 or force:
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             if backend == "nccl":
                 torch.cuda.set_device(self.local)
@@ -112,8 +115,8 @@ class Dist:
         return float(t.item())
 
     def close(self):
-        if self.world > 1:
-            import torch.distributed as dist
+        import torch.distributed as dist
+        if dist.is_initialized():
             dist.destroy_process_group()
 
 
@@ -260,6 +263,7 @@ def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
     if cl and x.dim() == 4:
         x = x.contiguous(memory_format=torch.channels_last)
     world = getattr(args, "world", 1)
+    dp = world > 1 or getattr(args, "dp", False)
     if opt_impl is not None:  # unfused torch.optim baseline (or no update at all)
         g = of.build_classifier(wl["model"], device=device, seed=seed, channels_last=bool(cl))
         if opt_impl == "none-mixed":   # our model math: bf16 module, no autocast, no update
@@ -274,7 +278,7 @@ def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
             if graphed and name in ("Adam", "AdamW"):
                 kw["capturable"] = True
             opt = getattr(torch.optim, name)(net.parameters(), **kw)
-        if world > 1:  # unfused data parallel: DDP all-reduce + torch.optim
+        if dp:  # unfused data parallel: DDP all-reduce + torch.optim
             net = torch.nn.parallel.DistributedDataParallel(net, device_ids=[device.index])
             graphed = False
         amp = torch.autocast("cuda", dtype=torch.bfloat16) if mixed else None
@@ -295,7 +299,7 @@ def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
                 opt.step()
             return loss
         owner, pol = net, opt
-    elif world > 1:  # data parallel: sharded fused update over NCCL
+    elif dp:  # data parallel: sharded fused update over NCCL
         from paper_2104_00237_b200.dp import DataParallelFusion
         g = of.build_classifier(wl["model"], device=device, seed=seed)
         g.track_counts = False
@@ -561,7 +565,7 @@ def run_ours(args) -> dict:
     import torch
 
     from paper_2104_00237_b200 import _native
-    dist = Dist().init("nccl")
+    dist = Dist().init("nccl", force=args.force_dp)
     device = torch.device("cuda", dist.local)
     torch.cuda.set_device(device)
     torch.backends.cudnn.benchmark = True
@@ -570,6 +574,7 @@ def run_ours(args) -> dict:
     torch.backends.cuda.matmul.allow_tf32 = True
     peaks = load_peaks()
     args.world = dist.world
+    args.dp = dist.world > 1 or args.force_dp
     flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=device)
     flush = flush_buf.zero_
 
@@ -599,9 +604,13 @@ def run_ours(args) -> dict:
            "config": {"workload": WORKLOAD, "model": args.model, "batch_per_gpu": args.batch,
                       "global_batch": args.batch * dist.world, "schedule": args.schedule,
                       "workers": args.workers, "grad_reset": args.grad_reset,
-                      "bucket_elems": args.bucket_elems, "cuda_graph": bool(args.graphs),
-                      "channels_last": bool(args.channels_last),
+                      "bucket_elems": args.bucket_elems,
+                      "cuda_graph": bool(args.graphs) and not args.dp,
+                      "channels_last": bool(args.channels_last) and not args.dp,
                       "parallelism": f"dp{dist.world}",
+                      "dp_path": ("sharded fused update: per-bucket NCCL reduce-scatter -> update "
+                                  "-> all-gather; unfused baseline DDP + torch.optim"
+                                  if args.dp else None),
                       "l2": "256 MiB buffer zeroed before every timed step (inside the timed region)",
                       "model_math": ("fp32 parameters/activations; TF32 tensor cores for convolutions "
                                      f"(cudnn.allow_tf32={torch.backends.cudnn.allow_tf32}) and matmuls "
@@ -613,7 +622,7 @@ def run_ours(args) -> dict:
         sched = {}
         for b in [args.batch] + [int(x) for x in args.sweep.split(",") if x.strip()]:
             row = {}
-            for name, sch, w, gr, opt, be, gph, cl in _variants_c2(dist.world):
+            for name, sch, w, gr, opt, be, gph, cl in _variants_c2(2 if args.dp else 1):
                 if b != args.batch and name not in SWEEP_ROWS:
                     continue
                 ts = []
@@ -646,11 +655,11 @@ def run_ours(args) -> dict:
         res["e2e"] = e2e(args, device, dist)
         # the kernel's own duration is a per-GPU quantity: measured on this
         # GPU's single-process engine whatever the world size
-        world, args.world = args.world, 1
+        world, dp, args.world, args.dp = args.world, args.dp, 1, False
         try:
             ins = measure_in_situ(args, device, peaks, 5)
         finally:
-            args.world = world
+            args.world, args.dp = world, dp
         std = measure_update_kernel(args, device, peaks)
         tr = ncu_traffic("c2_backward_fusion_buckets")
         res["roofline"] = {"bound": "hbm", "kernel": "mt_step_kernel (backward-fusion, side stream)",
@@ -715,7 +724,7 @@ def run_extra(args, wl: str, device, dist, flush) -> dict:
     steps, warm = max(args.steps // 3, 5), 3
     row, failed = {}, {}
     for name, sch, w, opt, be, gph in _variants_extra(wl):
-        if gph and dist.world > 1:
+        if gph and args.dp:
             continue
         try:
             st, *_ = make_runner(args, b, sch, device, workers=w, opt_impl=opt, bucket_elems=be,
