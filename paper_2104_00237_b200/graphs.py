@@ -20,8 +20,8 @@ advanced per replay so that flushes and checkpoints after replays see the
 right step; stepping the policy eagerly between replays is rejected.
 
 Constraints: inputs are copied into static buffers; a forward-fusion step
-must be captured with ``graph=`` so that its gradients can be kept resident
-across replays (``grad_reset`` is switched to "zero" for it, see __init__).
+must be captured with ``graph=``: the gradients one replay produces are what
+the next replay's forward reads, and the capture routes them (see __init__).
 """
 
 from __future__ import annotations
@@ -57,17 +57,23 @@ class CapturedStep:
         cur.wait_stream(side)
         torch.cuda.synchronize()
         # Forward fusion reads, in iteration i+1, the gradients iteration i
-        # produced.  Released gradients (grad_reset="none") would be
-        # re-allocated at other addresses by the next backward, and a replay
-        # would read the captured (stale) ones; keeping them allocated and
-        # zeroed in the update kernel makes the buffers the graph captured the
-        # ones every replay writes and reads.
+        # produced.  The captured forward-fusion launches read the gradients
+        # that exist now (the last warm-up iteration's); every replay's
+        # backward writes its gradients into the graph's own pool.  So the
+        # captured iteration ends with one multi-tensor copy of its gradients
+        # into the buffers the next replay's forward reads (held here).  With
+        # grad_reset="zero" the gradients are persistent and need nothing.
         self.grad_reset_forced = False
+        self._ff_prev = None
         owner = getattr(graph, "_flag_owner", None)
-        if (policy is not None and policy.grad_reset == "none" and owner is not None
-                and owner.num_pending() > 0):
-            policy.grad_reset = "zero"
-            self.grad_reset_forced = True
+        ff = owner is not None and owner.num_pending() > 0
+        if ff and policy is not None and policy.grad_reset == "none":
+            prev = [p.value.grad for p in graph.parameters]
+            if all(g is not None for g in prev):
+                self._ff_prev = prev
+            else:             # some parameter has no gradient: keep them resident instead
+                policy.grad_reset = "zero"
+                self.grad_reset_forced = True
         from . import _native, kernels
         self.dstep = None
         if policy is not None and policy.kind not in _STEP_INDEPENDENT:
@@ -86,6 +92,11 @@ class CapturedStep:
                     policy._dstep = None
             else:
                 self.loss = step_fn(self._arg())
+            if self._ff_prev is not None:
+                cur = [p.value.grad for p in graph.parameters]
+                if any(g is None for g in cur):
+                    raise StateError("forward fusion left a parameter without a gradient")
+                torch._foreach_copy_(self._ff_prev, cur)
         # liboptfuse_b200 kernel nodes in the graph (each replay launches them all)
         self.native_launches = _native.launch_count() - n0
         if self.dstep is not None:

@@ -379,7 +379,11 @@ def flush_pending_updates(graph: Graph, policy: OptimizerPolicy,
     if not todo:
         return 0
     if owner is not None:
-        eng = _engine(graph, policy, False)
+        # the engine that holds the flags (forward fusion with or without
+        # the side-stream lookahead uses different engines)
+        eng = next((e for e in graph._engines.values() if e.native is owner), None)
+        if eng is None:
+            eng = _engine(graph, policy, False)
         eng.configure(policy, graph.pending_step_t, graph.pending_scale)
         n = eng.native.flush()
     else:
