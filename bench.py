@@ -59,9 +59,12 @@ def parse_args(argv=None):
     ap.add_argument("--ff-bucket-elems", type=int, default=1 << 18,
                     help="forward-fusion buckets (0 = one pre-hook per layer)")
     ap.add_argument("--grad-reset", default="none", choices=("zero", "none"))
-    ap.add_argument("--bucket-elems", type=int, default=1 << 18,
+    ap.add_argument("--bucket-elems", type=int, default=1 << 20,
                     help="backward-fusion launch groups: 0 = one per layer, else merge layers "
-                         "(backward order) into buckets of at least this many elements")
+                         "(backward order) into buckets of at least this many elements (1M: "
+                         "MobileNetV2's 2.24 M parameters in 3 launches of >= 4 MB, the smallest "
+                         "size that leaves the kernel's ~4 us latency floor, still overlapped "
+                         "with the backward of the earlier layers)")
     ap.add_argument("--sweep", default="32,64,256,512", help="extra per-GPU batches ('' to skip)")
     ap.add_argument("--graphs", type=int, default=1,
                     help="1: capture each iteration (ours and the torch baseline) as a CUDA graph")
@@ -528,7 +531,11 @@ def _variants_c2(world: int):
 KEY_ROWS = ("torch.optim.SGD(foreach)", "ours:backward-fusion(w=2,bucket=256K)",
             "ours:forward-fusion(bucket=256K)", "graph:torch.optim.SGD(foreach)",
             "graph:ours:backward-fusion(w=2,bucket=256K)", "cl:graph:torch.optim.SGD(foreach)",
-            "cl:graph:ours:backward-fusion(w=2,bucket=256K)", "cl:graph:ours:forward-fusion(bucket=256K)")
+            "cl:graph:ours:backward-fusion(w=2,bucket=256K)", "cl:graph:ours:forward-fusion(bucket=256K)",
+            "cl:graph:ours:backward-fusion(w=2,bucket=1M)",
+            # the floors vary with cuDNN's per-instance algorithm choice as much as the rows
+            "fwd+bwd only (no update: lower bound)", "graph:fwd+bwd only (no update: lower bound)",
+            "cl:graph:fwd+bwd only (no update: lower bound)")
 SWEEP_ROWS = ("torch.optim.SGD(foreach)", "ours:forward-fusion(bucket=256K)",
               "graph:fwd+bwd only (no update: lower bound)",
               "ours:backward-fusion(w=2,bucket=256K)", "graph:torch.optim.SGD(foreach)",

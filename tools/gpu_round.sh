@@ -19,7 +19,7 @@ if [ -n "${NCU}" ]; then
   # launch under the profiler when it is a graph node
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "timed" -c 3000 --csv \
     --log-file gpurun_out/launches_eager.csv python bench.py --no-extras --graphs 0 --steps 4 --warmup 3 --instances 1 > gpurun_out/ncu_bench_eager.log 2>&1; echo ncu_list_eager=$?
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:mt_step -s 40 -c 8 \
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:mt_step -s 15 -c 3 \
     -o gpurun_out/prof_bf -f python tools/profile_kernels.py bf > gpurun_out/ncu_bf.log 2>&1; echo ncu_bf=$?
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:mt_step -s 1 -c 1 \
     -o gpurun_out/prof_vgg -f python tools/profile_kernels.py vgg > gpurun_out/ncu_vgg.log 2>&1; echo ncu_vgg=$?

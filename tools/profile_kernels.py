@@ -24,7 +24,7 @@ def bf(iters=6):
     x, y = synthetic_batch("mobilenet_v2_cifar", 128, device="cuda")
     x = x.contiguous(memory_format=torch.channels_last)
     for _ in range(iters):
-        of.run_backward_fusion(g, pol, (x, y), workers=2, bucket_elems=1 << 18, timing=False)  # headline groups
+        of.run_backward_fusion(g, pol, (x, y), workers=2, bucket_elems=1 << 20, timing=False)  # headline groups
     torch.cuda.synchronize()
 
 
