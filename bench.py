@@ -576,6 +576,10 @@ def run_ours(args) -> dict:
     device = torch.device("cuda", dist.local)
     torch.cuda.set_device(device)
     torch.backends.cudnn.benchmark = True
+    # try every cuDNN algorithm: with the default limit (10) the choice varies
+    # between model instances and ~1 instance in 4 lands 5-8% off the others
+    # (tools/cudnn_variance.py); with 0 every instance of every arm agrees
+    torch.backends.cudnn.benchmark_limit = 0
     # fp32 training on B200 the usual way: TF32 tensor cores for matmuls as
     # well as convolutions (cuDNN's default), for every arm alike
     torch.backends.cuda.matmul.allow_tf32 = True
