@@ -49,7 +49,7 @@ TRANSPORTS = ("nccl", "peer")
 
 class _Bucket:
     __slots__ = ("index", "params", "offsets", "flat_param", "flat_grad", "grad_shard", "slots",
-                 "shard", "master", "tl", "peer", "hparam", "hgrad", "ready", "event", "done", "leader", "pending")
+                 "shard", "master", "tl", "peer", "hparam", "hgrad", "sq_tl", "ready", "event", "done", "leader", "pending")
 
     def __init__(self, index):
         self.index = index
@@ -176,6 +176,26 @@ class DataParallelFusion:
         self.scale = None
         if self.cuda:
             self.scale = torch.full((), 1.0 / self.world, dtype=torch.float32, device=self.device)
+        # global-norm clipping (baseline / forward fusion; backward fusion
+        # rejects it): factor of the averaged gradient, folded with 1/W into
+        # the sharded updates' device gradient scale
+        self._clip_gscale = None
+        self._host_factor = None
+        if policy.clip_norm is not None and transport == "peer":
+            raise ConfigError("global-norm clipping needs the reduce-scattered shards "
+                              "(transport='nccl'): the peer kernel sums and updates in one pass")
+        if policy.clip_norm is not None and self.cuda:
+            dev = self.device
+            self._sq = torch.zeros((), dtype=torch.float64, device=dev)
+            self._factor = torch.zeros((), dtype=torch.float64, device=dev)
+            self._coef = torch.zeros((), dtype=torch.float32, device=dev)
+            self._clip_gscale = torch.zeros((), dtype=torch.float32, device=dev)
+            self._ws = torch.empty(kernels.sqnorm_workspace_len(), dtype=torch.float64, device=dev)
+            for b in self.buckets:
+                tl = kernels.TensorList(1)
+                tl.set(0, None, b.grad_shard)
+                tl.set_dtypes(torch.float32 if self.mixed else b.grad_shard.dtype, b.grad_shard.dtype)
+                b.sq_tl = tl
         self._hooks = None
         self._mode = None
         self._leader_handles = None
@@ -192,6 +212,35 @@ class DataParallelFusion:
         if self._sync is None:
             self._sync = h
         return t, h
+
+    # -- global-norm clipping ---------------------------------
+
+    def _clip(self) -> None:
+        """After every bucket's reduce-scatter: Σ g² over this rank's summed
+        gradient shards (f64, fixed order), one all-reduce of that scalar, the
+        norm of the averaged gradient sqrt(total) / W and the clip factor of
+        optim.py:165-168; the update kernels then multiply their summed
+        gradient by f32(factor) * (1/W)."""
+        W = self.world
+        if not self.cuda:   # host stand-in (gloo tests): same quantities in torch
+            total = torch.zeros((), dtype=torch.float64)
+            for b in self.buckets:
+                g = b.grad_shard.double()
+                total += (g * g).sum()
+            dist.all_reduce(total, group=self.group)
+            norm = float(total.sqrt()) / W
+            mx = self.policy.clip_norm
+            self._host_factor = 1.0 if norm <= mx else mx / norm
+            return
+        for i, b in enumerate(self.buckets):
+            kernels.sqnorm(b.sq_tl, self._ws, self._sq, i > 0, None)
+        dist.all_reduce(self._sq, group=self.group)
+        self._sq.div_(float(W * W))
+        kernels.clip_coef(self._sq, self.policy.clip_norm, self._coef, self._factor, None)
+        torch.mul(self._coef, 1.0 / W, out=self._clip_gscale)
+
+    def _gscale(self):
+        return self._clip_gscale if self._clip_gscale is not None else self.scale
 
     # -- the per-bucket pipeline ----------------------------------------------
 
@@ -225,14 +274,18 @@ class DataParallelFusion:
         if self.update_fn is not None:
             if self.mixed:    # host stand-in: fp32 grad shard, master updated, bf16 written back
                 g = b.grad_shard.float().mul_(1.0 / self.world)
+                if self._host_factor is not None:
+                    g.mul_(self._host_factor)
                 self.update_fn(b.master, g, b.slots, t)
                 with torch.no_grad():
                     b.flat_param[b.shard].copy_(b.master)
             else:
                 b.grad_shard.mul_(1.0 / self.world)
+                if self._host_factor is not None:
+                    b.grad_shard.mul_(self._host_factor)
                 self.update_fn(b.flat_param[b.shard], b.grad_shard, b.slots, t)
         else:
-            kernels.policy_step(b.tl, self.policy._hparams(t), self.scale,
+            kernels.policy_step(b.tl, self.policy._hparams(t), self._gscale(),
                                 self.flags | self.policy.device_step_flag, None)
         dist.all_gather_into_tensor(b.flat_param, b.flat_param[b.shard], group=self.group)
 
@@ -276,6 +329,9 @@ class DataParallelFusion:
         for b in self.buckets:
             if b.ready < len(b.params):  # parameters without gradients this iteration
                 self._bucket_ready(b)
+        if self.policy.clip_norm is not None:   # forward fusion: the deferred updates need it
+            with self._on_stream(self.comm):
+                self._clip()
         if self.cuda:
             self.join_event.record(self.comm)
             torch.cuda.current_stream().wait_event(self.join_event)
@@ -312,9 +368,16 @@ class DataParallelFusion:
         self.policy.begin_iteration()
         loss = self.graph.forward(inp)
         self.graph.backward()
-        for b in reversed(self.buckets):
-            self._reduce_scatter(b)
-            self._update_and_gather(b, self.policy.t)
+        if self.policy.clip_norm is not None:   # global information: every shard first
+            for b in reversed(self.buckets):
+                self._reduce_scatter(b)
+            self._clip()
+            for b in reversed(self.buckets):
+                self._update_and_gather(b, self.policy.t)
+        else:
+            for b in reversed(self.buckets):
+                self._reduce_scatter(b)
+                self._update_and_gather(b, self.policy.t)
         return StepReport("baseline", loss, None)
 
     def run_forward_fusion(self, inp, *, timing: bool = False):

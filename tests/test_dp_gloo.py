@@ -177,3 +177,75 @@ def test_sharded_mixed_precision_equals_single_process(schedule):
             assert full[off:off + w.size].tobytes() == w.tobytes()
             mask[off:off + w.size] = False
         assert not full[mask].any()     # alignment gaps and padding stay zero
+
+
+# -- global-norm clipping under data parallel --------------
+
+CLIP = 0.05
+
+
+def _worker_clip(rank, world, port, schedule, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2104_00237_b200 as of
+        from paper_2104_00237_b200.dp import DataParallelFusion
+        g = of.build_model("shared-chain", layers=4, width=6, device="cpu", exact=False,
+                           track_input_grad=False)
+        pol = of.OptimizerPolicy(KIND, eta=ETA, weight_decay=WD, clip_norm=CLIP)
+        dp = DataParallelFusion(g, pol, bucket_elems=40, update_fn=_oracle_update)
+        if schedule == "backward-fusion":
+            with pytest.raises(of.GlobalInfoRequired):
+                dp.run_backward_fusion(_inputs(rank)[0])
+            out[rank] = b""
+            return
+        run = {"baseline": dp.run_baseline, "forward-fusion": dp.run_forward_fusion}[schedule]
+        for x in _inputs(rank):
+            run(x)
+        dp.flush()
+        out[rank] = np.concatenate([p.value.detach().numpy().reshape(-1) for p in g.parameters]).tobytes()
+    finally:
+        dist.destroy_process_group()
+
+
+def _single_process_clip():
+    import paper_2104_00237_b200 as of
+    from oracle import optim_ref
+    g = of.build_model("shared-chain", layers=4, width=6, device="cpu", exact=False,
+                       track_input_grad=False)
+    hp = optim_ref.Hyper(kind=KIND, eta=ETA, weight_decay=WD)
+    slots = [dict() for _ in g.parameters]
+    xs = [_inputs(r) for r in range(2)]
+    for it in range(ITERS):
+        grads = []
+        for r in range(2):
+            for p in g.parameters:
+                p.value.grad = None
+            g.module(xs[r][it]).backward()
+            grads.append([p.value.grad.numpy().reshape(-1).copy() for p in g.parameters])
+        avg = [(grads[0][k] + grads[1][k]) * np.float32(0.5) for k in range(len(g.parameters))]
+        optim_ref.clip_by_global_norm(avg, CLIP)
+        for k, p in enumerate(g.parameters):
+            theta = p.value.detach().numpy().reshape(-1)
+            optim_ref.step(KIND, hp, theta, avg[k], slots[k], it + 1)
+    return np.concatenate([p.value.detach().numpy().reshape(-1) for p in g.parameters])
+
+
+@pytest.mark.parametrize("schedule", ["baseline", "forward-fusion", "backward-fusion"])
+def test_sharded_clip_matches_single_process(schedule):
+    """Baseline / forward fusion with a global-norm clip: one all-reduced f64
+    scalar per iteration, the factor of the averaged gradient; equal to the
+    single-process reference within the clip's own tolerance (its BLAS sdot
+    order is unspecified, optim.py:163).  Backward fusion refuses the policy
+    before touching anything."""
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().dict()
+    mp.start_processes(_worker_clip, args=(2, _free_port(), schedule, out), nprocs=2, join=True,
+                       start_method="spawn")
+    if schedule == "backward-fusion":
+        return
+    assert out[0] == out[1], "ranks disagree after the all-gather"
+    got = np.frombuffer(out[0], np.float32)
+    want = _single_process_clip()
+    assert np.allclose(got, want, rtol=1e-5, atol=1e-6), np.abs(got - want).max()
