@@ -663,7 +663,7 @@ def run_ours(args) -> dict:
                         ("c4", "c4_resnet50_bf16_adamw"), ("c5", "c5_bert_base_adamw")):
             if wl in args.extras.split(","):
                 res[key] = run_extra(args, wl, device, dist, flush)
-        res["e2e"] = e2e(args, device, dist)
+        res["e2e"] = e2e(args, device, dist, flush)
         # the kernel's own duration is a per-GPU quantity: measured on this
         # GPU's single-process engine whatever the world size
         world, dp, args.world, args.dp = args.world, args.dp, 1, False
@@ -770,10 +770,12 @@ def run_extra(args, wl: str, device, dist, flush) -> dict:
     return out
 
 
-def e2e(args, device, dist) -> dict:
+def e2e(args, device, dist, flush=None) -> dict:
     """The headline configuration through the public API, end to end: each
     step copies the batch from pinned host memory to the device and reads the
-    loss back (CapturedStep copies into its static buffers, then replays)."""
+    loss back (CapturedStep copies into its static buffers, then replays).
+    Wall clock over the K steps, max over ranks; L2 flushed before every step
+    like the device-timed value."""
     import torch
 
     from paper_2104_00237_b200.models import synthetic_batch
@@ -782,11 +784,15 @@ def e2e(args, device, dist) -> dict:
     step, g, pol = make_runner(args, args.batch, args.schedule, device)
     if hasattr(step, "graph"):
         def one():
+            if flush is not None:
+                flush()
             return step((xh, yh)).item()
     else:
         run = step.run
 
         def one():
+            if flush is not None:
+                flush()
             return run((xh.to(device, non_blocking=True), yh.to(device, non_blocking=True))).item()
     for _ in range(args.warmup):
         one()
