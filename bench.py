@@ -70,6 +70,9 @@ def parse_args(argv=None):
                     help="1: capture each iteration (ours and the torch baseline) as a CUDA graph")
     ap.add_argument("--channels-last", type=int, default=1, help="1: NHWC model and inputs")
     ap.add_argument("--no-extras", action="store_true", help="headline only (for profilers)")
+    ap.add_argument("--dp-graphs", type=int, default=0,
+                    help="1: capture data-parallel iterations (NCCL collectives included) as CUDA "
+                         "graphs too")
     ap.add_argument("--force-dp", action="store_true",
                     help="run the data-parallel code path (NCCL process group, DataParallelFusion, "
                          "DDP baselines) even at one GPU: the N>1 path's smoke test")
@@ -282,8 +285,9 @@ def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
                 kw["capturable"] = True
             opt = getattr(torch.optim, name)(net.parameters(), **kw)
         if dp:  # unfused data parallel: DDP all-reduce + torch.optim
-            net = torch.nn.parallel.DistributedDataParallel(net, device_ids=[device.index])
-            graphed = False
+            net = torch.nn.parallel.DistributedDataParallel(net, device_ids=[device.index],
+                                                            static_graph=bool(args.dp_graphs))
+            graphed = graphed and bool(args.dp_graphs)
         amp = torch.autocast("cuda", dtype=torch.bfloat16) if mixed else None
 
         def run(inp):
@@ -313,7 +317,7 @@ def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
         dpf = DataParallelFusion(g, pol)
         dp_run = {"baseline": dpf.run_baseline, "forward-fusion": dpf.run_forward_fusion,
                   "backward-fusion": dpf.run_backward_fusion}[schedule]
-        graphed = False
+        graphed = graphed and bool(args.dp_graphs)   # NCCL collectives captured in the graph
 
         def run(inp):
             return dp_run(inp).loss
@@ -489,7 +493,7 @@ def cpu_baseline(args, iters: int) -> dict:
                        f"over {r['update_elems']} params)")}
 
 
-def _variants_c2(world: int):
+def _variants_c2(world: int, dp_graphs: bool = False):
     """(name, schedule, workers, grad_reset, torch optimizer, bucket, CUDA graph, channels-last)"""
     K = 1 << 18
     LB = "fwd+bwd only (no update: lower bound)"
@@ -523,7 +527,7 @@ def _variants_c2(world: int):
          ("cl:graph:ours:forward-fusion(bucket=1M)", "forward-fusion", None, None, None, 4 * K, True, True),
          ("cl:graph:ours:forward-fusion(bucket=256K,prefetch)", "forward-fusion", 2, None, None, K, True, True),
          ("ours:forward-fusion(bucket=256K,prefetch)", "forward-fusion", 2, None, None, K, False, False)]
-    if world > 1:
+    if world > 1 and not dp_graphs:
         v = [x for x in v if not x[6]]
     return v
 
@@ -616,7 +620,7 @@ def run_ours(args) -> dict:
                       "global_batch": args.batch * dist.world, "schedule": args.schedule,
                       "workers": args.workers, "grad_reset": args.grad_reset,
                       "bucket_elems": args.bucket_elems,
-                      "cuda_graph": bool(args.graphs) and not args.dp,
+                      "cuda_graph": bool(args.graphs) and (not args.dp or bool(args.dp_graphs)),
                       "channels_last": bool(args.channels_last) and not args.dp,
                       "parallelism": f"dp{dist.world}",
                       "dp_path": ("sharded fused update: per-bucket NCCL reduce-scatter -> update "
@@ -633,7 +637,7 @@ def run_ours(args) -> dict:
         sched = {}
         for b in [args.batch] + [int(x) for x in args.sweep.split(",") if x.strip()]:
             row = {}
-            for name, sch, w, gr, opt, be, gph, cl in _variants_c2(2 if args.dp else 1):
+            for name, sch, w, gr, opt, be, gph, cl in _variants_c2(2 if args.dp else 1, bool(args.dp_graphs)):
                 if b != args.batch and name not in SWEEP_ROWS:
                     continue
                 ts = []
@@ -735,7 +739,7 @@ def run_extra(args, wl: str, device, dist, flush) -> dict:
     steps, warm = max(args.steps // 3, 5), 3
     row, failed = {}, {}
     for name, sch, w, opt, be, gph in _variants_extra(wl):
-        if gph and args.dp:
+        if gph and args.dp and not args.dp_graphs:
             continue
         try:
             st, *_ = make_runner(args, b, sch, device, workers=w, opt_impl=opt, bucket_elems=be,
