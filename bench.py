@@ -288,6 +288,8 @@ def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
             net = torch.nn.parallel.DistributedDataParallel(net, device_ids=[device.index],
                                                             static_graph=bool(args.dp_graphs))
             graphed = graphed and bool(args.dp_graphs)
+            if graphed:   # DDP logs runtime stats from Python in its first 10 iterations
+                net._set_ddp_runtime_logging_sample_rate(1 << 30)
         amp = torch.autocast("cuda", dtype=torch.bfloat16) if mixed else None
 
         def run(inp):
@@ -355,7 +357,8 @@ def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
         owner = g
     if graphed:
         ours = isinstance(pol, of.OptimizerPolicy)
-        cap = CapturedStep(run, (x, y), warmup=3, policy=pol if ours else None,
+        ddp = isinstance(owner, torch.nn.parallel.DistributedDataParallel)
+        cap = CapturedStep(run, (x, y), warmup=12 if ddp else 3, policy=pol if ours else None,
                            graph=owner if ours else None)
         return cap, owner, pol
 

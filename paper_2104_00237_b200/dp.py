@@ -424,11 +424,12 @@ class DataParallelFusion:
         bs = self._fwd_buckets
         b = bs[k]
         t = getattr(self, "_pending_t", None)
+        # a bucket made pending by the previous backward needs no wait: that
+        # backward ended with the compute stream joining the communication
+        # stream (and an event recorded then may predate a CUDA-graph capture)
         if b.pending:
-            if self.cuda:
-                torch.cuda.current_stream().wait_event(b.done)
             self._issue_deferred(b, t, None)
-        if self.cuda:
+        elif self.cuda:   # prefetched on the communication stream in this forward
             torch.cuda.current_stream().wait_event(b.done)
         if k + 1 < len(bs) and bs[k + 1].pending:   # prefetch the next bucket
             nb = bs[k + 1]
@@ -446,9 +447,7 @@ class DataParallelFusion:
     def _apply_deferred(self) -> None:
         t = getattr(self, "_pending_t", None)
         for b in self.buckets:
-            if b.pending:
-                if self.cuda:
-                    torch.cuda.current_stream().wait_event(b.done)
+            if b.pending:   # (ordered after its reduce-scatter by the backward's join)
                 self._update_and_gather(b, t)
                 b.pending = False
 
