@@ -284,12 +284,19 @@ def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
             if graphed and name in ("Adam", "AdamW"):
                 kw["capturable"] = True
             opt = getattr(torch.optim, name)(net.parameters(), **kw)
+        cap_stream = None
         if dp:  # unfused data parallel: DDP all-reduce + torch.optim
-            net = torch.nn.parallel.DistributedDataParallel(net, device_ids=[device.index],
-                                                            static_graph=bool(args.dp_graphs))
             graphed = graphed and bool(args.dp_graphs)
-            if graphed:   # DDP logs runtime stats from Python in its first 10 iterations
+            if graphed:   # DDP stashes autograd nodes on the stream it is built on: the capture's
+                cap_stream = torch.cuda.Stream()
+                cap_stream.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(cap_stream):
+                    net = torch.nn.parallel.DistributedDataParallel(
+                        net, device_ids=[device.index], static_graph=True)
+                # DDP logs runtime stats from Python in its first 10 iterations
                 net._set_ddp_runtime_logging_sample_rate(1 << 30)
+            else:
+                net = torch.nn.parallel.DistributedDataParallel(net, device_ids=[device.index])
         amp = torch.autocast("cuda", dtype=torch.bfloat16) if mixed else None
 
         def run(inp):
@@ -309,6 +316,7 @@ def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
             return loss
         owner, pol = net, opt
     elif dp:  # data parallel: sharded fused update over NCCL
+        cap_stream = None
         from paper_2104_00237_b200.dp import DataParallelFusion
         g = of.build_classifier(wl["model"], device=device, seed=seed)
         g.track_counts = False
@@ -325,6 +333,7 @@ def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
             return dp_run(inp).loss
         owner = g
     else:
+        cap_stream = None
         g = of.build_classifier(wl["model"], device=device, seed=seed, channels_last=bool(cl))
         g.track_counts = False  # no per-layer Python pre-hooks unless a schedule needs them
         if mixed:
@@ -359,7 +368,7 @@ def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
         ours = isinstance(pol, of.OptimizerPolicy)
         ddp = isinstance(owner, torch.nn.parallel.DistributedDataParallel)
         cap = CapturedStep(run, (x, y), warmup=12 if ddp else 3, policy=pol if ours else None,
-                           graph=owner if ours else None)
+                           graph=owner if ours else None, stream=cap_stream if ddp else None)
         return cap, owner, pol
 
     def step():
@@ -637,19 +646,25 @@ def run_ours(args) -> dict:
            "gpu_launches": int(launches)}
     res["config"]["instances_ms_per_step"] = [round(t, 4) for t in inst]
     if not args.no_extras:
-        sched = {}
+        sched, failed = {}, {}
         for b in [args.batch] + [int(x) for x in args.sweep.split(",") if x.strip()]:
             row = {}
             for name, sch, w, gr, opt, be, gph, cl in _variants_c2(2 if args.dp else 1, bool(args.dp_graphs)):
                 if b != args.batch and name not in SWEEP_ROWS:
                     continue
                 ts = []
-                for _ in range(args.instances if name in KEY_ROWS else 1):
-                    st, *_ = make_runner(args, b, sch, device, workers=w, grad_reset=gr, opt_impl=opt,
-                                         bucket_elems=be, graphed=gph, channels_last=cl)
-                    ts.append(timed(st, args.steps, args.warmup, dist, flush))
-                    del st
-                    torch.cuda.empty_cache()
+                try:
+                    for _ in range(args.instances if name in KEY_ROWS else 1):
+                        st, *_ = make_runner(args, b, sch, device, workers=w, grad_reset=gr,
+                                             opt_impl=opt, bucket_elems=be, graphed=gph,
+                                             channels_last=cl)
+                        ts.append(timed(st, args.steps, args.warmup, dist, flush))
+                        del st
+                        torch.cuda.empty_cache()
+                except Exception as e:  # noqa: BLE001 -- report, keep the other rows
+                    failed[f"{b}:{name}"] = f"{type(e).__name__}: {str(e).splitlines()[0][:160] if str(e) else ''}"
+                    torch.cuda.synchronize()
+                    continue
                 t = statistics.median(ts)
                 row[name] = {"ms_per_step": round(t, 4), "images_per_s": round(dist.world * b * 1e3 / t, 1)}
                 if len(ts) > 1:
@@ -657,15 +672,21 @@ def run_ours(args) -> dict:
             _speedups(row)
             sched[str(b)] = row
         res["schedules"] = sched
-        row = sched[str(args.batch)]
-        mode = ("cl:" if args.channels_last else "") + ("graph:" if args.graphs else "")
-        same = row.get(mode + "torch.optim.SGD(foreach)") or row["torch.optim.SGD(foreach)"]
+        if failed:
+            res["failed_rows"] = failed
+        row = sched.get(str(args.batch), {})
+        headline_graphed = bool(args.graphs) and (not args.dp or bool(args.dp_graphs))
+        mode = (("cl:" if args.channels_last and not args.dp else "")
+                + ("graph:" if headline_graphed else ""))
+        same = row.get(mode + "torch.optim.SGD(foreach)") or row.get("torch.optim.SGD(foreach)")
+        eager = row.get("torch.optim.SGD(foreach)")
         lb = row.get(mode + "fwd+bwd only (no update: lower bound)")
         res["vs_unfused_torch"] = {
-            "mode": mode or "eager", "torch_foreach_ms": same["ms_per_step"],
-            "speedup": round(same["ms_per_step"] / ms, 4),
+            "mode": mode or "eager",
+            "torch_foreach_ms": same["ms_per_step"] if same else None,
+            "speedup": round(same["ms_per_step"] / ms, 4) if same else None,
             "fwd_bwd_only_ms": lb["ms_per_step"] if lb else None,
-            "speedup_vs_eager_torch_foreach": round(row["torch.optim.SGD(foreach)"]["ms_per_step"] / ms, 4)}
+            "speedup_vs_eager_torch_foreach": round(eager["ms_per_step"] / ms, 4) if eager else None}
         for wl, key in (("c1", "c1_resnet18_sgdm"), ("c3", "c3_vgg16_adam"),
                         ("c4", "c4_resnet50_bf16_adamw"), ("c5", "c5_bert_base_adamw")):
             if wl in args.extras.split(","):

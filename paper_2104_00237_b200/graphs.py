@@ -43,13 +43,16 @@ class CapturedStep:
     ``pending_step_t`` in step with the replays).
     """
 
-    def __init__(self, step_fn, static_inputs, policy=None, warmup: int = 3, graph=None):
+    def __init__(self, step_fn, static_inputs, policy=None, warmup: int = 3, graph=None,
+                 stream=None):
         self.static = static_inputs if isinstance(static_inputs, tuple) else (static_inputs,)
         self.step_fn = step_fn
         self.policy = policy
         self.owner = graph
         cur = torch.cuda.current_stream()
-        side = torch.cuda.Stream()
+        # warm-up and capture stream (a caller whose module stashed autograd
+        # nodes on a stream, e.g. DDP, passes that stream)
+        side = stream if stream is not None else torch.cuda.Stream()
         side.wait_stream(cur)
         with torch.cuda.stream(side):
             for _ in range(warmup):
@@ -82,7 +85,7 @@ class CapturedStep:
             torch.cuda.synchronize()
         n0 = _native.launch_count()
         self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph):
+        with torch.cuda.graph(self.graph, stream=side):
             if self.dstep is not None:
                 kernels.step_advance(self.dstep.offset, 1)   # first node of every replay
                 policy._dstep = self.dstep
