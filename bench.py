@@ -318,13 +318,13 @@ def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
     elif dp:  # data parallel: sharded fused update over NCCL
         cap_stream = None
         from paper_2104_00237_b200.dp import DataParallelFusion
-        g = of.build_classifier(wl["model"], device=device, seed=seed)
+        g = of.build_classifier(wl["model"], device=device, seed=seed, channels_last=bool(cl))
         g.track_counts = False
         if mixed:
             g.use_master_weights()
             x = x.to(torch.bfloat16) if x.is_floating_point() else x
         pol = of.OptimizerPolicy(wl["kind"], **wl["hp"])
-        dpf = DataParallelFusion(g, pol)
+        dpf = DataParallelFusion(g, pol, bucket_elems=bucket_elems or args.bucket_elems)
         dp_run = {"baseline": dpf.run_baseline, "forward-fusion": dpf.run_forward_fusion,
                   "backward-fusion": dpf.run_backward_fusion}[schedule]
         graphed = graphed and bool(args.dp_graphs)   # NCCL collectives captured in the graph
@@ -633,7 +633,7 @@ def run_ours(args) -> dict:
                       "workers": args.workers, "grad_reset": args.grad_reset,
                       "bucket_elems": args.bucket_elems,
                       "cuda_graph": bool(args.graphs) and (not args.dp or bool(args.dp_graphs)),
-                      "channels_last": bool(args.channels_last) and not args.dp,
+                      "channels_last": bool(args.channels_last),
                       "parallelism": f"dp{dist.world}",
                       "dp_path": ("sharded fused update: per-bucket NCCL reduce-scatter -> update "
                                   "-> all-gather; unfused baseline DDP + torch.optim"
@@ -676,7 +676,7 @@ def run_ours(args) -> dict:
             res["failed_rows"] = failed
         row = sched.get(str(args.batch), {})
         headline_graphed = bool(args.graphs) and (not args.dp or bool(args.dp_graphs))
-        mode = (("cl:" if args.channels_last and not args.dp else "")
+        mode = (("cl:" if args.channels_last else "")
                 + ("graph:" if headline_graphed else ""))
         same = row.get(mode + "torch.optim.SGD(foreach)") or row.get("torch.optim.SGD(foreach)")
         eager = row.get("torch.optim.SGD(foreach)")

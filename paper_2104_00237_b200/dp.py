@@ -124,14 +124,17 @@ class DataParallelFusion:
             with torch.no_grad():
                 for p, off in zip(b.params, b.offsets):
                     v = p.value
-                    if not v.is_contiguous():
-                        raise ConfigError(f"parameter {p.id} must be contiguous for data parallel")
-                    k = v.numel()
-                    b.flat_param[off:off + k].copy_(v.reshape(-1))
+                    if not _dense(v):
+                        raise ConfigError(f"parameter {p.id} must be dense (contiguous or "
+                                          "channels-last) for data parallel")
+                    # views with the parameter's own strides: a channels-last
+                    # weight keeps its memory layout inside the flat buffer
+                    pv = torch.as_strided(b.flat_param, v.size(), v.stride(), off)
+                    pv.copy_(v)
                     if self.mixed:
-                        flat_master[off:off + k].copy_(p.master.reshape(-1))
-                    v.data = b.flat_param[off:off + k].view_as(v)
-                    v.grad = b.flat_grad[off:off + k].view_as(v)
+                        torch.as_strided(flat_master, v.size(), v.stride(), off).copy_(p.master)
+                    v.data = pv
+                    v.grad = torch.as_strided(b.flat_grad, v.size(), v.stride(), off)
             if self.mixed:
                 dist.broadcast(flat_master, src=src, group=group)
                 with torch.no_grad():
@@ -455,6 +458,15 @@ class DataParallelFusion:
         n = sum(len(b.params) for b in self.buckets if b.pending)
         self._apply_deferred()
         return n
+
+
+def _dense(t) -> bool:
+    """Non-overlapping and dense: the elements fill [0, numel) of its storage
+    span in some stride order (contiguous, channels-last, ...)."""
+    if t.is_contiguous() or t.is_contiguous(memory_format=torch.channels_last):
+        return True
+    from torch._prims_common import is_non_overlapping_and_dense
+    return is_non_overlapping_and_dense(t)
 
 
 class _NullCtx:
