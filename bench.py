@@ -70,9 +70,9 @@ def parse_args(argv=None):
                     help="1: capture each iteration (ours and the torch baseline) as a CUDA graph")
     ap.add_argument("--channels-last", type=int, default=1, help="1: NHWC model and inputs")
     ap.add_argument("--no-extras", action="store_true", help="headline only (for profilers)")
-    ap.add_argument("--dp-graphs", type=int, default=0,
+    ap.add_argument("--dp-graphs", type=int, default=1,
                     help="1: capture data-parallel iterations (NCCL collectives included) as CUDA "
-                         "graphs too")
+                         "graphs too (0: eager data parallel)")
     ap.add_argument("--force-dp", action="store_true",
                     help="run the data-parallel code path (NCCL process group, DataParallelFusion, "
                          "DDP baselines) even at one GPU: the N>1 path's smoke test")
@@ -610,9 +610,19 @@ def run_ours(args) -> dict:
     # median over --instances independently built instances, each timed for
     # exactly K steps after W warm-up steps.
     inst = []
+    dp_graph_error = None
     with Clocks(dist.local) as clk:
         for _ in range(args.instances):
-            step, g, pol = make_runner(args, args.batch, args.schedule, device)
+            try:
+                step, g, pol = make_runner(args, args.batch, args.schedule, device)
+            except Exception as e:  # noqa: BLE001
+                if not (args.dp and args.dp_graphs):
+                    raise
+                # data-parallel capture failed: measure the eager data-parallel step
+                args.dp_graphs = 0
+                dp_graph_error = f"{type(e).__name__}: {str(e).splitlines()[0][:160] if str(e) else ''}"
+                torch.cuda.synchronize()
+                step, g, pol = make_runner(args, args.batch, args.schedule, device)
             n0 = _native.launch_count()
             inst.append(timed(step, args.steps, args.warmup, dist, flush))
             if hasattr(step, "native_launches"):   # CUDA graph: kernel nodes replayed per step
@@ -645,6 +655,8 @@ def run_ours(args) -> dict:
                                      "optimizer update exact fp32 (reference arithmetic)")},
            "gpu_launches": int(launches)}
     res["config"]["instances_ms_per_step"] = [round(t, 4) for t in inst]
+    if dp_graph_error:
+        res["config"]["dp_graph_capture_failed"] = dp_graph_error
     if not args.no_extras:
         sched, failed = {}, {}
         for b in [args.batch] + [int(x) for x in args.sweep.split(",") if x.strip()]:
