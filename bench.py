@@ -505,6 +505,25 @@ def cpu_baseline(args, iters: int) -> dict:
                        f"over {r['update_elems']} params)")}
 
 
+def cpu_update_baseline(std: dict) -> dict:
+    """The reference update alone on this host (numpy oracle port, 1 thread)
+    next to the kernel's standalone pass over each config's parameter set."""
+    from oracle import timing
+    rates = {"sgd-momentum": timing.reference_update_rate("sgd-momentum",
+                                                         dict(eta=0.1, alpha=0.9, weight_decay=5e-4)),
+             "adam": timing.reference_update_rate("adam", dict(eta=1e-4, weight_decay=1e-4))}
+    out = {"kind": "port", "cores": 1, "rates": rates, "configs": {}}
+    for name, kind in (("vgg16_adam", "adam"), ("bert_base_adamw", "adam"),
+                       ("resnet50_bf16_master_adamw", "adam"), ("mobilenet_v2_sgdm", "sgd-momentum")):
+        if name not in std:
+            continue
+        elems = std[name]["bytes"] / 28 if kind == "adam" else std[name]["bytes"] / 20
+        cpu_ms = elems / rates[kind]["elems_per_s"] * 1e3
+        out["configs"][name] = {"cpu_ms": round(cpu_ms, 1), "gpu_us": std[name]["us"],
+                                "ratio": round(cpu_ms * 1e3 / std[name]["us"], 1)}
+    return out
+
+
 def _variants_c2(world: int, dp_graphs: bool = False):
     """(name, schedule, workers, grad_reset, torch optimizer, bucket, CUDA graph, channels-last)"""
     K = 1 << 18
@@ -724,6 +743,7 @@ def run_ours(args) -> dict:
                            "standalone_single_launch": std}
         if dist.rank == 0 and dist.world == 1:
             res["cpu_baseline"] = cpu_baseline(args, args.cpu_iters)
+            res["cpu_update_baseline"] = cpu_update_baseline(std)
     res["clocks"] = clocks
     dist.close()
     return res

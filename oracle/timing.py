@@ -60,3 +60,23 @@ def cpu_training_sample(model_name: str, batch: int, iters: int, kind: str, hp: 
     return {"images_per_s": batch / per_iter, "ms_per_iter": per_iter * 1e3,
             "fwd_bwd_ms": float(np.mean(fb)) * 1e3, "update_ms": float(np.mean(upd)) * 1e3,
             "update_elems": n_elem, "threads": threads, "batch": batch, "iters": iters}
+
+
+def reference_update_rate(kind: str, hp: dict, elems: int = 1 << 22, reps: int = 3) -> dict:
+    """Throughput of the reference update alone (OptimizerPolicy.step restated
+    in numpy, one thread as in the reference) on one ``elems``-element f32
+    tensor: elements/s and algorithmic GB/s (same byte model as the kernels)."""
+    rng = np.random.default_rng(0)
+    theta = rng.standard_normal(elems).astype(np.float32)
+    h = optim_ref.Hyper(kind=kind, **hp)
+    slots: dict = {}
+    ts = []
+    for t in range(1, reps + 2):
+        grad = (rng.standard_normal(elems) * 0.01).astype(np.float32)
+        t0 = time.perf_counter()
+        optim_ref.step(kind, h, theta, grad, slots, t)
+        ts.append(time.perf_counter() - t0)
+    sec = float(np.median(ts[1:]))
+    bpe = 4 * (2 + 2 * len(optim_ref.SLOTS[kind])) + 4
+    return {"elems_per_s": elems / sec, "gbs": elems * bpe / sec / 1e9, "threads": 1,
+            "sample": f"{reps} steps of one {elems}-element f32 tensor"}
