@@ -10,13 +10,14 @@ Layout (per bucket = consecutive layers in backward order, ``launch_groups``):
   flat_param [padded]  -- the module's parameters become views into it, each
                           starting on a 128-byte boundary (gaps stay zero:
                           a zero gradient on a zero parameter updates to zero)
-  flat_grad  [padded]  -- ``param.grad`` views; AccumulateGrad adds in place
+  flat_grad  [padded]  -- gradients copied in per bucket (one multi-tensor copy;
+                          AccumulateGrad keeps stealing its input)
   grad_shard [S], history shards [S] per slot, S = padded / W (padded to W*4
   elements so every shard starts 16-byte aligned for the vector path)
 
 Backward fusion: when the last gradient of a bucket is accumulated, the
 bucket's pipeline is issued on the communication stream behind an event:
-``reduce_scatter_tensor(SUM)`` -> zero flat_grad -> the multi-tensor update
+copy gradients in -> ``reduce_scatter_tensor(SUM)`` -> the multi-tensor update
 kernel on the shard (1/W folded in as the device gradient scale) ->
 ``all_gather_into_tensor`` back into flat_param.  It overlaps the backward of
 the remaining layers; the compute stream joins once at the end of backward.
@@ -49,7 +50,8 @@ TRANSPORTS = ("nccl", "peer")
 
 class _Bucket:
     __slots__ = ("index", "params", "offsets", "flat_param", "flat_grad", "grad_shard", "slots",
-                 "shard", "master", "tl", "peer", "hparam", "hgrad", "sq_tl", "ready", "event", "done", "leader", "pending")
+                 "shard", "master", "tl", "peer", "hparam", "hgrad", "sq_tl", "grad_views", "ready",
+                 "event", "done", "leader", "pending")
 
     def __init__(self, index):
         self.index = index
@@ -134,7 +136,10 @@ class DataParallelFusion:
                     if self.mixed:
                         torch.as_strided(flat_master, v.size(), v.stride(), off).copy_(p.master)
                     v.data = pv
-                    v.grad = torch.as_strided(b.flat_grad, v.size(), v.stride(), off)
+                    v.grad = None
+            # where each parameter's gradient lands in flat_grad (same strides)
+            b.grad_views = [torch.as_strided(b.flat_grad, p.value.size(), p.value.stride(), off)
+                            for p, off in zip(b.params, b.offsets)]
             if self.mixed:
                 dist.broadcast(flat_master, src=src, group=group)
                 with torch.no_grad():
@@ -247,11 +252,32 @@ class DataParallelFusion:
 
     # -- the per-bucket pipeline ----------------------------------------------
 
+    def _gather_grads(self, b) -> None:
+        """Copy the bucket's gradients into flat_grad with one multi-tensor copy
+        and release them.  AccumulateGrad steals each incoming gradient
+        (``p.grad`` is None), where persistent views into flat_grad would cost
+        one add kernel per parameter per step (+0.3 ms on MobileNetV2 in a
+        CUDA graph).  Alignment gaps and padding are never written: zero."""
+        dst, src = [], []
+        for p, view in zip(b.params, b.grad_views):
+            g = p.value.grad
+            if g is None:          # no contribution this iteration: the reference steps with 0
+                view.zero_()
+                continue
+            dst.append(view)
+            src.append(g)
+        if src:
+            torch._foreach_copy_(dst, src)
+        for p, g in zip(b.params, [p.value.grad for p in b.params]):
+            if g is not None and self.cuda:
+                g.record_stream(torch.cuda.current_stream())   # freed after this stream's copy
+            p.value.grad = None
+
     def _reduce_scatter(self, b) -> None:
+        self._gather_grads(b)
         if self.transport == "peer":
             return   # the fused kernel reads every peer's gradients in place
         dist.reduce_scatter_tensor(b.grad_shard, b.flat_grad, op=dist.ReduceOp.SUM, group=self.group)
-        b.flat_grad.zero_()
 
     def _update_and_gather(self, b, t: int) -> None:
         if self.transport == "peer":
