@@ -19,5 +19,15 @@ from .schedule import (BACKWARD_FUSION, BASELINE, FORWARD_FUSION, SCHEDULES,
                        flush_pending_updates, run_backward_fusion, run_baseline,
                        run_forward_fusion)
 from .trace import ScheduleTrace, critical_path_depth, validate_trace
+from . import checkpoint  # noqa: E402  (state_dict / load_state_dict / observe)
+from .graphs import CapturedStep
 
-__version__ = "0.1.0"
+__version__ = "0.2.0"
+
+
+def __getattr__(name):
+    # torch.distributed is only imported when data parallel is asked for
+    if name == "DataParallelFusion":
+        from .dp import DataParallelFusion
+        return DataParallelFusion
+    raise AttributeError(name)
