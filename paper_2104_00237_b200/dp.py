@@ -85,6 +85,7 @@ class DataParallelFusion:
             raise ConfigError("the sharded update runs on CUDA; pass update_fn only for host tests")
         self.comm = torch.cuda.Stream() if self.cuda else None
         self._sync = None
+        self.barrier_timeout_ms = 0   # peer transport: 0 = wait indefinitely
         slots = policy.history_slots()
         # mixed precision (C4): the module runs in bf16 with fp32 masters
         # (Graph.use_master_weights).  Gradients are reduce-scattered in bf16;
@@ -293,10 +294,10 @@ class DataParallelFusion:
             if not on_comm:
                 self.comm.wait_stream(cur)
             with torch.cuda.stream(self.comm):
-                self._sync.barrier(channel=0)
+                self._sync.barrier(channel=0, timeout_ms=self.barrier_timeout_ms)
                 kernels.dp_step_peer(b.peer, self.policy._hparams(t), self.scale,
                                      self.policy.device_step_flag, None)
-                self._sync.barrier(channel=0)
+                self._sync.barrier(channel=0, timeout_ms=self.barrier_timeout_ms)
             if not on_comm:
                 cur.wait_stream(self.comm)
             return

@@ -1,0 +1,103 @@
+"""The peer transport with REAL ranks on ONE GPU (diagnostic / GPU test
+helper): W processes share cuda:0, a gloo process group carries the
+rendezvous, torch symmetric memory maps each rank's buffers into the others
+(CUDA IPC on the same device), and the barriers order the ranks.  Each rank
+trains the exact (fixed-order) chain with backward fusion on its own input;
+afterwards every rank's parameters must equal the reference update applied
+to the rank-averaged gradient (numpy oracle), bit for bit.
+
+    python tools/peer_w2_one_gpu.py [W]        # prints one JSON line
+"""
+
+import json
+import os
+import socket
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as mp  # noqa: E402
+
+KIND, ETA, WD, ITERS, LAYERS, WIDTH = "adam", 1e-2, 1e-3, 3, 4, 8
+
+
+def _inputs(rank):
+    rng = np.random.default_rng(100 + rank)
+    return [rng.uniform(0.1, 1.0, (3, WIDTH)).astype(np.float32) for _ in range(ITERS)]
+
+
+def _worker(rank, world, port, schedule, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2104_00237_b200 as of
+        from paper_2104_00237_b200.dp import DataParallelFusion
+        g = of.build_model("chain", layers=LAYERS, width=WIDTH, seed=0, device="cuda")
+        pol = of.OptimizerPolicy(KIND, eta=ETA, weight_decay=WD)
+        dpf = DataParallelFusion(g, pol, bucket_elems=2 * WIDTH * WIDTH, transport="peer")
+        dpf.barrier_timeout_ms = 60_000
+        run = {"backward-fusion": dpf.run_backward_fusion, "baseline": dpf.run_baseline,
+               "forward-fusion": dpf.run_forward_fusion}[schedule]
+        for x in _inputs(rank):
+            run(torch.from_numpy(x).cuda())
+        dpf.flush()
+        torch.cuda.synchronize()
+        out[rank] = np.concatenate([p.value.detach().cpu().numpy().reshape(-1)
+                                    for p in g.parameters]).tobytes()
+    finally:
+        dist.destroy_process_group()
+
+
+def _reference(world):
+    from oracle import chain_ref, optim_ref
+    m = chain_ref.build("chain", layers=LAYERS, width=WIDTH, seed=0)
+    h = optim_ref.Hyper(kind=KIND, eta=ETA, weight_decay=WD)
+    slots = [dict() for _ in m.params]
+    xs = [_inputs(r) for r in range(world)]
+    def grads_of(x):
+        for g in m.grads:
+            g[:] = 0
+        _, saved = chain_ref._forward(m, x)
+        gout = None
+        for i in reversed(range(len(m.layer_param))):
+            gout = chain_ref._backward_node(m, i, saved, gout)
+        return [g.copy() for g in m.grads]
+
+    for it in range(ITERS):
+        grads = [grads_of(xs[r][it]) for r in range(world)]
+        for k, theta in enumerate(m.params):
+            g = grads[0][k].copy()
+            for r in range(1, world):
+                g = np.add(g, grads[r][k])
+            g = np.multiply(g, np.float32(1.0 / world))
+            optim_ref.step(KIND, h, theta, g, slots[k], it + 1)
+    return np.concatenate(m.params).tobytes()
+
+
+def main():
+    world = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+    res = {}
+    for schedule in ("backward-fusion", "baseline", "forward-fusion"):
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        out = mp.get_context("spawn").Manager().dict()
+        mp.start_processes(_worker, args=(world, port, schedule, out), nprocs=world, join=True,
+                           start_method="spawn")
+        same = all(out[r] == out[0] for r in range(world))
+        want = _reference(world)
+        got = np.frombuffer(out[0], np.float32)
+        ref = np.frombuffer(want, np.float32)
+        res[schedule] = {"ranks_agree": same, "bitwise_vs_oracle": out[0] == want,
+                         "max_abs_err": float(np.abs(got - ref).max())}
+    print(json.dumps({"world": world, **res}))
+
+
+if __name__ == "__main__":
+    main()
