@@ -1,10 +1,14 @@
 """The peer transport with REAL ranks on ONE GPU (diagnostic / GPU test
-helper): W processes share cuda:0, a gloo process group carries the
-rendezvous, torch symmetric memory maps each rank's buffers into the others
-(CUDA IPC on the same device), and the barriers order the ranks.  Each rank
-trains the exact (fixed-order) chain with backward fusion on its own input;
-afterwards every rank's parameters must equal the reference update applied
-to the rank-averaged gradient (numpy oracle), bit for bit.
+helper): W processes share cuda:0 and a gloo process group.  torch symmetric
+memory refuses two ranks on one device, so the flat buffers are mapped into
+the other ranks with CUDA IPC (torch's own tensor-sharing handles, exchanged
+with all_gather_object) and the cross-rank barrier is a host barrier after a
+device synchronize.  Everything else is the product path: DataParallelFusion
+with transport="peer", the of_dp_step_peer kernel reading and writing the
+other processes' buffers through their IPC mappings.  Each rank trains the
+exact (fixed-order) chain on its own input; every rank's parameters must
+equal the reference update applied to the rank-averaged gradient (numpy
+oracle), bit for bit.
 
     python tools/peer_w2_one_gpu.py [W]        # prints one JSON line
 """
@@ -37,11 +41,43 @@ def _worker(rank, world, port, schedule, out):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import paper_2104_00237_b200 as of
+        from paper_2104_00237_b200 import dp as dp_mod
         from paper_2104_00237_b200.dp import DataParallelFusion
+        from torch.multiprocessing.reductions import reduce_tensor
+
+        class _HostBarrier:
+            def __init__(self, ptrs):
+                self.buffer_ptrs = ptrs
+
+            def barrier(self, channel=0, timeout_ms=0):
+                torch.cuda.synchronize()
+                dist.barrier()
+                torch.cuda.synchronize()
+
+        keep = []
+
+        def _ipc_symmetric(self, n, dt):
+            t = torch.zeros(n, dtype=dt, device=self.device)
+            fn, args = reduce_tensor(t)
+            handles = [None] * self.world
+            dist.all_gather_object(handles, args)
+            ptrs = []
+            for r, a in enumerate(handles):
+                if r == self.rank:
+                    ptrs.append(t.data_ptr())
+                else:
+                    peer = fn(*a)        # cudaIpcOpenMemHandle in this process
+                    keep.append(peer)
+                    ptrs.append(peer.data_ptr())
+            h = _HostBarrier(ptrs)
+            if self._sync is None:
+                self._sync = h
+            return t, h
+
+        dp_mod.DataParallelFusion._symmetric = _ipc_symmetric
         g = of.build_model("chain", layers=LAYERS, width=WIDTH, seed=0, device="cuda")
         pol = of.OptimizerPolicy(KIND, eta=ETA, weight_decay=WD)
         dpf = DataParallelFusion(g, pol, bucket_elems=2 * WIDTH * WIDTH, transport="peer")
-        dpf.barrier_timeout_ms = 60_000
         run = {"backward-fusion": dpf.run_backward_fusion, "baseline": dpf.run_baseline,
                "forward-fusion": dpf.run_forward_fusion}[schedule]
         for x in _inputs(rank):
