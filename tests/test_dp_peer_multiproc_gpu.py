@@ -1,0 +1,27 @@
+"""The data-parallel peer transport with real ranks: W processes share the one
+GPU, their flat buffers are mapped into each other with CUDA IPC
+(tools/peer_w2_one_gpu.py), and of_dp_step_peer reads and writes the other
+processes' memory.  Every schedule must leave every rank with the reference
+update of the rank-averaged gradient, bit for bit (exact chain model)."""
+
+import json
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parent.parent
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_transport_real_ranks_one_gpu(world):
+    proc = subprocess.run([sys.executable, str(ROOT / "tools" / "peer_w2_one_gpu.py"), str(world)],
+                          capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert proc.returncode == 0, proc.stderr[-2000:]
+    res = json.loads(proc.stdout.strip().splitlines()[-1])
+    assert res["world"] == world
+    for sched in ("backward-fusion", "baseline", "forward-fusion"):
+        assert res[sched]["ranks_agree"], sched
+        assert res[sched]["bitwise_vs_oracle"], (sched, res[sched]["max_abs_err"])
