@@ -1,7 +1,8 @@
-"""The data-parallel peer transport with real ranks: W processes share the one
-GPU, their flat buffers are mapped into each other with CUDA IPC
-(tools/peer_w2_one_gpu.py), and of_dp_step_peer reads and writes the other
-processes' memory.  Every schedule must leave every rank with the reference
+"""Data parallel with real ranks: W processes share the one GPU
+(tools/peer_w2_one_gpu.py).  Peer transport: their flat buffers are mapped into
+each other with CUDA IPC and of_dp_step_peer reads and writes the other
+processes' memory.  Collectives transport: the reduce-scatter / all-gather
+run over gloo on the CUDA tensors around the sharded kernel.  Every schedule must leave every rank with the reference
 update of the rank-averaged gradient, bit for bit (exact chain model)."""
 
 import json
@@ -15,9 +16,13 @@ pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parent.parent
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_peer_transport_real_ranks_one_gpu(world):
-    proc = subprocess.run([sys.executable, str(ROOT / "tools" / "peer_w2_one_gpu.py"), str(world)],
+@pytest.mark.parametrize("world,mode", [(2, "peer"), (3, "peer"), (2, "collectives")])
+def test_data_parallel_real_ranks_one_gpu(world, mode):
+    """mode "peer": the fused peer kernel over CUDA-IPC mappings; "collectives":
+    reduce-scatter -> sharded kernel -> all-gather with the collectives carried
+    by gloo on the CUDA tensors (NCCL refuses two ranks on one device)."""
+    proc = subprocess.run([sys.executable, str(ROOT / "tools" / "peer_w2_one_gpu.py"), str(world),
+                           mode],
                           capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert proc.returncode == 0, proc.stderr[-2000:]
     res = json.loads(proc.stdout.strip().splitlines()[-1])

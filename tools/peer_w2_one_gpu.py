@@ -35,7 +35,7 @@ def _inputs(rank):
     return [rng.uniform(0.1, 1.0, (3, WIDTH)).astype(np.float32) for _ in range(ITERS)]
 
 
-def _worker(rank, world, port, schedule, out):
+def _worker(rank, world, port, schedule, out, transport="peer"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -77,7 +77,7 @@ def _worker(rank, world, port, schedule, out):
         dp_mod.DataParallelFusion._symmetric = _ipc_symmetric
         g = of.build_model("chain", layers=LAYERS, width=WIDTH, seed=0, device="cuda")
         pol = of.OptimizerPolicy(KIND, eta=ETA, weight_decay=WD)
-        dpf = DataParallelFusion(g, pol, bucket_elems=2 * WIDTH * WIDTH, transport="peer")
+        dpf = DataParallelFusion(g, pol, bucket_elems=2 * WIDTH * WIDTH, transport=transport)
         run = {"backward-fusion": dpf.run_backward_fusion, "baseline": dpf.run_baseline,
                "forward-fusion": dpf.run_forward_fusion}[schedule]
         for x in _inputs(rank):
@@ -118,21 +118,24 @@ def _reference(world):
 
 def main():
     world = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+    # "collectives": the reduce-scatter -> sharded kernel -> all-gather path, its
+    # collectives carried by the gloo group (NCCL refuses two ranks on one GPU)
+    transport = "nccl" if len(sys.argv) > 2 and sys.argv[2] == "collectives" else "peer"
     res = {}
     for schedule in ("backward-fusion", "baseline", "forward-fusion"):
         with socket.socket() as s:
             s.bind(("127.0.0.1", 0))
             port = s.getsockname()[1]
         out = mp.get_context("spawn").Manager().dict()
-        mp.start_processes(_worker, args=(world, port, schedule, out), nprocs=world, join=True,
-                           start_method="spawn")
+        mp.start_processes(_worker, args=(world, port, schedule, out, transport), nprocs=world,
+                           join=True, start_method="spawn")
         same = all(out[r] == out[0] for r in range(world))
         want = _reference(world)
         got = np.frombuffer(out[0], np.float32)
         ref = np.frombuffer(want, np.float32)
         res[schedule] = {"ranks_agree": same, "bitwise_vs_oracle": out[0] == want,
                          "max_abs_err": float(np.abs(got - ref).max())}
-    print(json.dumps({"world": world, **res}))
+    print(json.dumps({"world": world, "transport": transport, **res}))
 
 
 if __name__ == "__main__":
