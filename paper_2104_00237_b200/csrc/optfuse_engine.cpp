@@ -215,9 +215,20 @@ class Engine : public std::enable_shared_from_this<Engine> {
       callback_(idx);
     }
     const int gi = group_of_[idx];
-    if (gi < 0 || !launch_) return;
+    if (gi < 0) return;
+    if (!launch_) {
+      // readiness only: the group callback (data-parallel buckets) runs once
+      // per complete group instead of Python once per parameter
+      if (group_cb_ && ++ready_[gi] == static_cast<int>(groups_[gi].members.size())) {
+        py::gil_scoped_acquire gil;
+        group_cb_(gi);
+      }
+      return;
+    }
     if (++ready_[gi] == static_cast<int>(groups_[gi].members.size())) launch_group(gi);
   }
+
+  void set_group_callback(py::object cb) { group_cb_ = cb.is_none() ? py::object() : cb; }
 
   // Launch every group that did not complete during backward (parameters
   // that received no gradient this iteration still step, with g = 0, as the
@@ -511,7 +522,7 @@ class Engine : public std::enable_shared_from_this<Engine> {
   bool profile_ = false;
   std::vector<ProfRec> prof_;
   int64_t launches_ = 0;
-  py::object callback_;
+  py::object callback_, group_cb_;
 };
 
 void FusionHook::operator()(const Variable&) {
@@ -531,6 +542,7 @@ PYBIND11_MODULE(_optfuse_engine, m) {
       .def("install_hooks", &Engine::install_hooks)
       .def("remove_hooks", &Engine::remove_hooks)
       .def("set_callback", &Engine::set_callback)
+      .def("set_group_callback", &Engine::set_group_callback)
       .def("bf_begin", &Engine::bf_begin, py::arg("launch") = true)
       .def("disarm", &Engine::disarm)
       .def("bf_finish", &Engine::bf_finish)

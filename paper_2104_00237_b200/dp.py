@@ -327,11 +327,43 @@ class DataParallelFusion:
     def _install(self) -> None:
         if self._hooks is not None:
             return
+        if self.cuda:
+            # the native engine's C++ gradient-ready hooks count readiness per
+            # bucket and call back into Python once per bucket (not once per
+            # parameter); no launches of its own
+            from .engine import native_engine_module
+            g = self.graph
+            eng = native_engine_module().Engine(
+                [p.value for p in g.parameters], [[p.id for p in b.params] for b in self.buckets],
+                [[p.id for p in L.params] for L in g.layers], 0)
+            eng.set_group_callback(self._on_bucket_ready)
+            eng.install_hooks()
+            g._hook_owner = eng
+            self._eng = eng
+            self._hooks = [eng]
+            return
         hooks = []
         for p in self.graph.parameters:
             hooks.append(p.value.register_post_accumulate_grad_hook(
                 lambda t, p=p: self._on_grad_ready(p)))
         self._hooks = hooks
+
+    def _on_bucket_ready(self, gi: int) -> None:
+        b = self.buckets[gi]
+        if self._mode is None:
+            return
+        b.ready = len(b.params)
+        self._bucket_ready(b)
+
+    def _backward(self) -> None:
+        eng = getattr(self, "_eng", None)
+        if eng is not None:
+            eng.bf_begin(False)
+        try:
+            self.graph.backward()
+        finally:
+            if eng is not None:
+                eng.disarm()
 
     def _on_grad_ready(self, p) -> None:
         b = self.bucket_of.get(p.id)
@@ -382,10 +414,7 @@ class DataParallelFusion:
         pol.begin_iteration()
         loss = self.graph.forward(inp)
         self._mode = "backward-fusion"
-        try:
-            self.graph.backward()
-        finally:
-            pass
+        self._backward()
         self._finish_backward()
         self._mode = None
         return StepReport("backward-fusion", loss, None, fused=True)
@@ -420,10 +449,7 @@ class DataParallelFusion:
         loss = self.graph.forward(inp)
         self._apply_deferred()          # buckets whose leader did not run
         self._mode = "forward-fusion"
-        try:
-            self.graph.backward()
-        finally:
-            pass
+        self._backward()
         self._finish_backward()
         self._mode = None
         self._pending_t = self.policy.t
