@@ -183,6 +183,14 @@ typedef struct of_peer_bucket {
 int of_dp_step_peer(const of_peer_bucket* bucket, const of_hparams* hp,
                     const float* grad_scale_dev, uint32_t flags, void* stream);
 
+/* Parity-harness helper (not on the update path): out[M][N] = a[M][K] @ b[K][N]
+ * (row-major, contiguous) with the reference engine's fixed accumulation order
+ * (tensor.py: out = 0; out = out + a[:, k] * b[k, :] for k ascending, every
+ * product and sum correctly rounded), so the synthetic graphs' gradients are
+ * bit-identical to the reference's.  dtype: OF_F32 or OF_F64; M <= 65535. */
+int of_exact_matmul(const void* a, const void* b, void* out, int64_t M, int64_t K, int64_t N,
+                    int dtype, void* stream);
+
 /* Sum of squares of every grad in `list`, accumulated in f64 with a fixed
  * (deterministic) reduction order (optim.py:160-164).  Uses `workspace_dev`
  * (>= of_sqnorm_workspace_len() doubles).  Writes *out_dev = sum, or

@@ -512,6 +512,21 @@ __global__ void clip_coef_kernel(const double* sq, double max_norm, float* coef,
 
 __global__ void step_advance_kernel(int64_t* offset, int64_t delta) { *offset += delta; }
 
+// Fixed-order matmul of the synthetic parity graphs (tensor.py's
+// accumulation: out = 0; for k ascending: out = out + a[:, k] * b[k, :], every
+// product and sum separately rounded): one thread per output element.
+template <class T>
+__global__ void __launch_bounds__(kThreads)
+exact_matmul_kernel(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ out,
+                    int64_t M, int64_t K, int64_t N) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
+  const int64_t i = blockIdx.y;
+  if (j >= N || i >= M) return;
+  T acc = T(0);
+  for (int64_t k = 0; k < K; ++k) acc = o_add(acc, o_mul(a[i * K + k], b[k * N + j]));
+  out[i * N + j] = acc;
+}
+
 // ---------------------------------------------------------------------------
 // Host side: validation, packing, dispatch.
 // ---------------------------------------------------------------------------
@@ -886,6 +901,27 @@ int of_step_advance(int64_t* step_offset_dev, int64_t delta, void* stream) {
   if (!step_offset_dev) return fail(OF_ERR_INVALID, "step_offset_dev is NULL");
   step_advance_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(step_offset_dev, delta);
   return check_launch("step_advance_kernel");
+}
+
+int of_exact_matmul(const void* a, const void* b, void* out, int64_t M, int64_t K, int64_t N,
+                    int dtype, void* stream) {
+  g_err[0] = '\0';
+  if (!a || !b || !out) return fail(OF_ERR_INVALID, "exact_matmul: NULL operand");
+  if (M < 0 || K < 0 || N < 0 || M > 65535)
+    return fail(OF_ERR_INVALID, "exact_matmul: bad shape %lld x %lld x %lld", (long long)M,
+                (long long)K, (long long)N);
+  if (M == 0 || N == 0) return OF_OK;
+  const dim3 grid(static_cast<unsigned>((N + kThreads - 1) / kThreads), static_cast<unsigned>(M));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (dtype == OF_F32)
+    exact_matmul_kernel<float><<<grid, kThreads, 0, s>>>(static_cast<const float*>(a),
+        static_cast<const float*>(b), static_cast<float*>(out), M, K, N);
+  else if (dtype == OF_F64)
+    exact_matmul_kernel<double><<<grid, kThreads, 0, s>>>(static_cast<const double*>(a),
+        static_cast<const double*>(b), static_cast<double*>(out), M, K, N);
+  else
+    return fail(OF_ERR_UNSUPPORTED, "exact_matmul: dtype %d", dtype);
+  return check_launch("exact_matmul_kernel");
 }
 
 int64_t of_sqnorm_workspace_len(void) { return kSqnormWorkspace; }

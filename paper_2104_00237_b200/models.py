@@ -44,7 +44,20 @@ def seeded_uniform(shape, lo: float, hi: float, seed: int, precision: str = "f32
 
 def fixed_order_matmul(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
     """a @ b accumulated one rank-1 product per contraction index, ascending,
-    each product and sum a separately rounded IEEE operation."""
+    each product and sum a separately rounded IEEE operation (tensor.py's
+    order).  On the GPU one kernel (``of_exact_matmul``) computes it; the host
+    loop serves the CPU-side tests of the synthetic graphs."""
+    if a.is_cuda and a.dtype in (torch.float32, torch.float64) and a.shape[0] <= 65535:
+        from . import _native as nat
+        from .kernels import _handle
+        a = a.contiguous()
+        b = b.contiguous()
+        out = torch.empty(a.shape[0], b.shape[1], dtype=a.dtype, device=a.device)
+        code = nat.OF_F32 if a.dtype == torch.float32 else nat.OF_F64
+        st = nat.lib().of_exact_matmul(a.data_ptr(), b.data_ptr(), out.data_ptr(), a.shape[0],
+                                       a.shape[1], b.shape[1], code, _handle(None))
+        nat.check(st, "of_exact_matmul")
+        return out
     out = torch.zeros(a.shape[0], b.shape[1], dtype=a.dtype, device=a.device)
     for k in range(a.shape[1]):
         out = out + a[:, k:k + 1] * b[k:k + 1, :]

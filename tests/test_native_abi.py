@@ -99,6 +99,9 @@ def test_invalid_arguments_rejected_before_launch():
     assert so.of_dp_step_peer(pb.ref, ctypes.byref(sgdm), None, 0, None) == nat.OF_ERR_INVALID
     assert so.of_dp_step_peer(pb.ref, ctypes.byref(sgdm), None, nat.OF_FLAG_ZERO_GRAD,
                               None) == nat.OF_ERR_INVALID
+    assert so.of_exact_matmul(None, 0x10, 0x20, 2, 2, 2, nat.OF_F32, None) == nat.OF_ERR_INVALID
+    assert so.of_exact_matmul(0x10, 0x10, 0x20, 70000, 2, 2, nat.OF_F32, None) == nat.OF_ERR_INVALID
+    assert so.of_exact_matmul(0x10, 0x10, 0x20, 2, 2, 2, nat.OF_BF16, None) == nat.OF_ERR_UNSUPPORTED
     empty = kernels.TensorList(0)
     assert so.of_policy_step_mt(empty.ref, ctypes.byref(hp), None, 0, None) == nat.OF_OK
     assert so.of_clip_coef(None, 1.0, None, None, None) == nat.OF_ERR_INVALID
