@@ -5,19 +5,27 @@
 
 Workload (N=1): configs[1] of BASELINE.json -- MobileNetV2 on synthetic
 CIFAR-10-shaped data (3x32x32, 10 classes), SGD-momentum (lr 0.1, momentum
-0.9, weight decay 5e-4), fp32, batch 128 per GPU, backward-fusion with the
-update on the side stream.  One "step" = one training iteration (forward,
-backward, every parameter updated).  The same iteration is also timed under
-the unfused PyTorch optimizer (torch.optim.SGD, foreach and fused) and under
-our baseline / forward-fusion / inline backward-fusion schedules; the batch
-sweep 32..512 is reported beside the headline.
+0.9, weight decay 5e-4), fp32 weights (TF32 convolutions and matmuls), batch
+128 per GPU, channels-last, backward fusion with 1M-element buckets on the
+side stream, the whole iteration replayed from a CUDA graph.  One "step" =
+one training iteration (forward, backward, every parameter updated), with a
+256 MiB L2 flush before it.  The same iteration is also timed with
+torch.optim.SGD (foreach, fused), with no update at all (the floor any fusion
+can reach), and under our other schedules, eager and graphed; a batch sweep
+32..512 and the other BASELINE.json configs (C1, C3, C4, C5) are reported
+beside the headline.  N>1 (torchrun): the data-parallel path (dp.py, NCCL
+reduce-scatter -> sharded update -> all-gather per bucket, captured in the
+graph) against DDP + torch.optim; --force-dp runs that path at N=1.
 
 Prints ONE JSON line (rank 0).  ``value`` = images/s over all ranks with
-inputs resident in HBM, device-timed with CUDA events (max over ranks);
-``e2e`` = the same through the public API with pinned-host inputs copied in
-and the loss read back every step; ``roofline`` = the update kernel's
-achieved algorithmic HBM bandwidth (events around each side-stream launch in
-an instrumented pass) against MEASURED_PEAKS.json; ``cpu_baseline`` = the
+inputs resident in HBM, device-timed with CUDA events (max over ranks),
+median of 3 independently built instances; ``e2e`` = the same through the
+public API with pinned-host inputs copied in and the loss read back every
+step; ``roofline`` = the update kernel's average launch duration on its
+stream (back-to-back replay of one iteration's launches) as algorithmic HBM
+bandwidth against MEASURED_PEAKS.json, with the ncu DRAM traffic per launch
+(profiles/ncu_traffic.json) and standalone single-pass figures for the
+C2-C5 parameter sets; ``cpu_baseline`` / ``cpu_update_baseline`` = the
 reference's CPU path (oracle port) on the host cores.
 
 ``--impl reference`` times the reference's CPU implementation of the path
