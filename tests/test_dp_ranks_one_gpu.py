@@ -1,5 +1,5 @@
 """Data parallel with real ranks: W processes share the one GPU
-(tools/peer_w2_one_gpu.py).  Peer transport: their flat buffers are mapped into
+(tools/dp_ranks_one_gpu.py).  Peer transport: their flat buffers are mapped into
 each other with CUDA IPC and of_dp_step_peer reads and writes the other
 processes' memory.  Collectives transport: the reduce-scatter / all-gather
 run over gloo on the CUDA tensors around the sharded kernel.  Every schedule must leave every rank with the reference
@@ -21,7 +21,7 @@ def test_data_parallel_real_ranks_one_gpu(world, mode):
     """mode "peer": the fused peer kernel over CUDA-IPC mappings; "collectives":
     reduce-scatter -> sharded kernel -> all-gather with the collectives carried
     by gloo on the CUDA tensors (NCCL refuses two ranks on one device)."""
-    proc = subprocess.run([sys.executable, str(ROOT / "tools" / "peer_w2_one_gpu.py"), str(world),
+    proc = subprocess.run([sys.executable, str(ROOT / "tools" / "dp_ranks_one_gpu.py"), str(world),
                            mode],
                           capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert proc.returncode == 0, proc.stderr[-2000:]

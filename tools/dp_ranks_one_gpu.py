@@ -10,7 +10,7 @@ exact (fixed-order) chain on its own input; every rank's parameters must
 equal the reference update applied to the rank-averaged gradient (numpy
 oracle), bit for bit.
 
-    python tools/peer_w2_one_gpu.py [W]        # prints one JSON line
+    python tools/dp_ranks_one_gpu.py [W]        # prints one JSON line
 """
 
 import json
