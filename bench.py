@@ -359,7 +359,9 @@ def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
                 return of.run_baseline(g, pol, inp, timing=False).loss
         elif schedule == "forward-fusion":
             fbe = args.ff_bucket_elems if bucket_elems is None else bucket_elems
-            pre = workers == 2   # forward fusion: an explicit workers=2 selects the side-stream lookahead
+            # forward fusion: an explicit workers=2 selects the side-stream lookahead of one
+            # unit, workers=-3 every unit at the first layer
+            pre = {2: 1, -3: -1}.get(workers, 0)
 
             def run(inp):
                 return of.run_forward_fusion(g, pol, inp, timing=False, bucket_elems=fbe,
@@ -570,6 +572,7 @@ def _variants_c2(world: int, dp_graphs: bool = False):
          ("cl:graph:ours:backward-fusion(w=1,bucket=256K)", "backward-fusion", 1, None, None, K, True, True),
          ("cl:graph:ours:forward-fusion(bucket=1M)", "forward-fusion", None, None, None, 4 * K, True, True),
          ("cl:graph:ours:forward-fusion(bucket=256K,prefetch)", "forward-fusion", 2, None, None, K, True, True),
+         ("cl:graph:ours:forward-fusion(bucket=256K,prefetch=all)", "forward-fusion", -3, None, None, K, True, True),
          ("ours:forward-fusion(bucket=256K,prefetch)", "forward-fusion", 2, None, None, K, False, False)]
     if world > 1 and not dp_graphs:
         v = [x for x in v if not x[6]]

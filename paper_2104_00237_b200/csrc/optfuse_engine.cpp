@@ -302,7 +302,7 @@ class Engine : public std::enable_shared_from_this<Engine> {
   // prefetch by an event, and the released gradients are held until the
   // compute stream has waited, so the allocator cannot hand them to the
   // forward while the side stream still reads them.
-  int ff_unit_lookahead(int u) {
+  int ff_unit_lookahead(int u, int depth = 1) {
     if (!side_) return ff_layer(u);
     const int nu = static_cast<int>(ff_units_.size());
     if (prefetch_done_.size() != static_cast<size_t>(nu)) {
@@ -321,7 +321,9 @@ class Engine : public std::enable_shared_from_this<Engine> {
     } else {
       n = ff_layer(u);
     }
-    if (u + 1 < nu) n += prefetch_unit(u + 1, cur);
+    // units u+1 .. u+depth (each issued once; prefetch_unit skips updated ones)
+    for (int v = u + 1; v < nu && v <= u + depth; ++v)
+      if (!prefetched_[v]) n += prefetch_unit(v, cur);
     return n;
   }
 
@@ -555,7 +557,7 @@ PYBIND11_MODULE(_optfuse_engine, m) {
       .def("set_updated", &Engine::set_updated)
       .def("num_pending", &Engine::num_pending)
       .def("ff_layer", &Engine::ff_layer)
-      .def("ff_unit_lookahead", &Engine::ff_unit_lookahead)
+      .def("ff_unit_lookahead", &Engine::ff_unit_lookahead, py::arg("u"), py::arg("depth") = 1)
       .def("ff_join", &Engine::ff_join)
       .def("set_ff_units", &Engine::set_ff_units)
       .def("reset_ff_units", &Engine::reset_ff_units)

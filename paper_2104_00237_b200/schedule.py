@@ -263,7 +263,7 @@ def ff_units(graph: Graph, bucket_elems: int) -> tuple:
 
 def run_forward_fusion(graph: Graph, policy: OptimizerPolicy, inp, *, timing: bool = True,
                        trace: bool = False, bucket_elems: int = 0,
-                       prefetch: bool = False) -> StepReport:
+                       prefetch: int = 0) -> StepReport:
     """Lazy schedule: deferred updates applied just before each layer's forward.
 
     The layer's forward pre-hook calls the native engine, which launches the
@@ -279,32 +279,40 @@ def run_forward_fusion(graph: Graph, policy: OptimizerPolicy, inp, *, timing: bo
     issued together right before the bucket's first layer, so only bucket
     leaders carry a pre-hook.
 
-    ``prefetch=True`` (B200 addition) issues unit u+1's update on a side
-    stream when unit u's pre-hook runs, so it overlaps unit u's forward; unit
-    u+1's pre-hook waits for it.  Same trajectory, bit for bit.
+    ``prefetch=d`` (B200 addition; True = 1) issues the updates of units
+    u+1 .. u+d on a side stream when unit u's pre-hook runs, so they overlap
+    the forward of the units before them; each unit's pre-hook waits for its
+    own update.  ``prefetch=-1``: every unit at the first pre-hook.  Same
+    trajectory, bit for bit.
     """
     _reject_newton(policy)
     checkpoint.attach(graph, policy)
     if bucket_elems < 0:
         raise ConfigError(f"bucket_elems must be >= 0, got {bucket_elems}")
     tc = tr.ScheduleTrace(FORWARD_FUSION) if trace else None
-    prefetch = prefetch and tc is None
+    depth = 0 if tc is not None else (1 << 30 if prefetch is not True and prefetch < 0
+                                      else int(prefetch))
+    prefetch = depth > 0
     eng = _engine(graph, policy, prefetch)
     graph.set_flag_owner(eng.native)
     policy.begin_iteration()
     if graph.pending_step_t is not None:
         eng.configure(policy, graph.pending_step_t, graph.pending_scale)
     native = eng.native
-    ff_layer = native.ff_unit_lookahead if prefetch else native.ff_layer
+    if prefetch:
+        def ff_layer(u, _f=native.ff_unit_lookahead, _d=depth):
+            return _f(u, _d)
+    else:
+        ff_layer = native.ff_layer
     if prefetch and bucket_elems == 0:
         bucket_elems = 1   # lookahead follows the recorded execution order: one unit per layer
     bucketed = bucket_elems > 0 and tc is None and graph.exec_order is not None
     if bucketed:
-        if eng.ff_bucket_elems != bucket_elems or eng.ff_prefetch != prefetch:
+        if eng.ff_bucket_elems != bucket_elems or eng.ff_prefetch != depth:
             units, leaders = ff_units(graph, bucket_elems)
             native.set_ff_units(units)
             eng.ff_bucket_elems = bucket_elems
-            eng.ff_prefetch = prefetch
+            eng.ff_prefetch = depth
             eng.ff_leaders = [(L, (lambda i=i: ff_layer(i))) for i, L in enumerate(leaders)]
         graph.set_leader_hooks(eng.ff_leaders)
         apply_pending = None
