@@ -18,8 +18,9 @@ import bench  # noqa: E402
 def main():
     limit = int(sys.argv[1]) if len(sys.argv) > 1 else 10
     n = int(sys.argv[2]) if len(sys.argv) > 2 else 6
-    torch.backends.cudnn.benchmark = True
-    torch.backends.cudnn.benchmark_limit = limit
+    # limit < 0: no benchmarking at all (cuDNN's heuristics pick)
+    torch.backends.cudnn.benchmark = limit >= 0
+    torch.backends.cudnn.benchmark_limit = max(limit, 0)
     torch.backends.cuda.matmul.allow_tf32 = True
     args = bench.parse_args(["--steps", "30", "--warmup", "10"])
     args.world, args.dp = 1, False
