@@ -778,7 +778,10 @@ def _variants_extra(wl: str):
          ("ours:baseline", "baseline", None, None, 0, False),
          ("ours:forward-fusion(per-layer)", "forward-fusion", None, None, 0, False),
          ("ours:backward-fusion(w=2,per-layer)", "backward-fusion", 2, None, 0, False),
-         ("ours:backward-fusion(w=2,per-layer,default-prio)", "backward-fusion", -2, None, 0, False)]
+         ("ours:backward-fusion(w=2,per-layer,default-prio)", "backward-fusion", -2, None, 0, False),
+         # inline on the autograd stream: each update right behind its layer's backward,
+         # gradients (and the weights dgrad just read) still in L2 -- the paper's locality
+         ("ours:backward-fusion(w=1,per-layer)", "backward-fusion", 1, None, 0, False)]
     if WORKLOADS[wl].get("mixed"):
         v.append((OWN_LB, "baseline", None, "none-mixed", 0, False))
     if wl == "c3":
@@ -795,7 +798,8 @@ def _variants_extra(wl: str):
           ("graph:ours:baseline", "baseline", None, None, 0, True),
           ("graph:ours:forward-fusion(bucket=1M)", "forward-fusion", None, None, 1 << 20, True),
           ("graph:ours:forward-fusion(bucket=1M,prefetch)", "forward-fusion", 2, None, 1 << 20, True),
-          ("graph:ours:backward-fusion(w=2,bucket=1M)", "backward-fusion", 2, None, 1 << 20, True)]
+          ("graph:ours:backward-fusion(w=2,bucket=1M)", "backward-fusion", 2, None, 1 << 20, True),
+          ("graph:ours:backward-fusion(w=1,per-layer)", "backward-fusion", 1, None, 0, True)]
     if WORKLOADS[wl].get("mixed"):
         v.append(("graph:" + OWN_LB, "baseline", None, "none-mixed", 0, True))
     return v
