@@ -183,6 +183,11 @@ typedef struct of_peer_bucket {
 int of_dp_step_peer(const of_peer_bucket* bucket, const of_hparams* hp,
                     const float* grad_scale_dev, uint32_t flags, void* stream);
 
+/* dst[i] <- src[i] (nbytes[i] bytes each) for n tensors in one launch per 256
+ * (multi-tensor copy; CUDA-graph forward fusion routes each replay's gradients
+ * to the buffers the next replay's updates read with it). */
+int of_copy_mt(void* const* dst, const void* const* src, const int64_t* nbytes, int n, void* stream);
+
 /* Parity-harness helper (not on the update path): out[M][N] = a[M][K] @ b[K][N]
  * (row-major, contiguous) with the reference engine's fixed accumulation order
  * (tensor.py: out = 0; out = out + a[:, k] * b[k, :] for k ascending, every

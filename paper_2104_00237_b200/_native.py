@@ -30,7 +30,8 @@ KIND_CODES = {"sgd": 0, "sgd-momentum": 1, "adagrad": 2, "rmsprop": 3, "adadelta
 # every symbol include/optfuse_b200.h declares (checked by tests/test_native_abi.py)
 SYMBOLS = ("of_abi_version", "of_status_string", "of_last_error", "of_launch_count",
            "of_policy_step_mt", "of_sgdm_mt", "of_adam_mt", "of_step_advance", "of_dp_step_peer",
-           "of_sqnorm_workspace_len", "of_sqnorm_mt", "of_clip_coef", "of_exact_matmul")
+           "of_sqnorm_workspace_len", "of_sqnorm_mt", "of_clip_coef", "of_exact_matmul",
+           "of_copy_mt")
 
 _vp = ctypes.c_void_p
 _PP = ctypes.POINTER(ctypes.c_void_p)
@@ -100,6 +101,8 @@ def lib():
     so.of_dp_step_peer.restype = ctypes.c_int
     so.of_dp_step_peer.argtypes = [ctypes.POINTER(OfPeerBucket), ctypes.POINTER(OfHparams), _vp,
                                    ctypes.c_uint32, _vp]
+    so.of_copy_mt.restype = ctypes.c_int
+    so.of_copy_mt.argtypes = [_PP, _PP, ctypes.POINTER(ctypes.c_int64), ctypes.c_int, _vp]
     so.of_exact_matmul.restype = ctypes.c_int
     so.of_exact_matmul.argtypes = [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                    ctypes.c_int, _vp]

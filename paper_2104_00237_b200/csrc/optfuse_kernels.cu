@@ -512,6 +512,34 @@ __global__ void clip_coef_kernel(const double* sq, double max_norm, float* coef,
 
 __global__ void step_advance_kernel(int64_t* offset, int64_t delta) { *offset += delta; }
 
+// Multi-tensor byte copy (dst[i] <- src[i]): one launch for a whole gradient
+// set.  MTParams carries dst in p, src in g and the byte count in n; tiles of
+// kCopyTile bytes, 16-byte vectors where both sides allow, bytes otherwise.
+constexpr int kCopyTile = 16384;
+template <int CAP>
+__global__ void __launch_bounds__(kThreads)
+mt_copy_kernel(const __grid_constant__ MTParams<CAP> mp) {
+  const int total = mp.tile_end[mp.count - 1];
+  int ti = 0;
+  for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+    ti = find_tensor(mp, ti, tile);
+    const int tfirst = ti ? mp.tile_end[ti - 1] : 0;
+    const int64_t base = static_cast<int64_t>(tile - tfirst) * kCopyTile;
+    const int64_t rem = mp.n[ti] - base;
+    const int len = rem < kCopyTile ? static_cast<int>(rem) : kCopyTile;
+    char* d = static_cast<char*>(mp.p[ti]) + base;
+    const char* s = static_cast<const char*>(mp.g[ti]) + base;
+    int from = 0;
+    if (aligned(d, 16) && aligned(s, 16)) {
+      const int nv = len / 16;
+      for (int j = threadIdx.x; j < nv; j += kThreads)
+        reinterpret_cast<uint4*>(d)[j] = reinterpret_cast<const uint4*>(s)[j];
+      from = nv * 16;
+    }
+    for (int j = from + threadIdx.x; j < len; j += kThreads) d[j] = s[j];
+  }
+}
+
 // Fixed-order matmul of the synthetic parity graphs (tensor.py's
 // accumulation: out = 0; for k ascending: out = out + a[:, k] * b[k, :], every
 // product and sum separately rounded): one thread per output element.
@@ -922,6 +950,37 @@ int of_exact_matmul(const void* a, const void* b, void* out, int64_t M, int64_t 
   else
     return fail(OF_ERR_UNSUPPORTED, "exact_matmul: dtype %d", dtype);
   return check_launch("exact_matmul_kernel");
+}
+
+int of_copy_mt(void* const* dst, const void* const* src, const int64_t* nbytes, int n, void* stream) {
+  g_err[0] = '\0';
+  if (n < 0 || (n > 0 && (!dst || !src || !nbytes))) return fail(OF_ERR_INVALID, "copy_mt: bad list");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (int first = 0; first < n; first += kCapMax) {
+    const int count = n - first < kCapMax ? n - first : kCapMax;
+    MTParams<kCapMax> mp;
+    memset(&mp, 0, sizeof(mp));
+    int64_t tiles = 0;
+    mp.count = count;
+    for (int i = 0; i < count; ++i) {
+      const int k = first + i;
+      if (nbytes[k] < 0) return fail(OF_ERR_INVALID, "copy_mt: tensor %d has %lld bytes", k,
+                                     (long long)nbytes[k]);
+      if (nbytes[k] > 0 && (!dst[k] || !src[k])) return fail(OF_ERR_INVALID, "copy_mt: NULL tensor %d", k);
+      mp.p[i] = dst[k];
+      mp.g[i] = const_cast<void*>(src[k]);
+      mp.n[i] = nbytes[k];
+      tiles += (nbytes[k] + kCopyTile - 1) / kCopyTile;
+      mp.tile_end[i] = static_cast<int32_t>(tiles);
+    }
+    if (tiles == 0) continue;
+    const int64_t cap = static_cast<int64_t>(sm_count()) * kCtasPerSm;
+    const int grid = static_cast<int>(tiles < cap ? tiles : cap);
+    mt_copy_kernel<kCapMax><<<grid, kThreads, 0, s>>>(mp);
+    const int st = check_launch("mt_copy_kernel");
+    if (st != OF_OK) return st;
+  }
+  return OF_OK;
 }
 
 int64_t of_sqnorm_workspace_len(void) { return kSqnormWorkspace; }

@@ -268,7 +268,10 @@ class DataParallelFusion:
             dst.append(view)
             src.append(g)
         if src:
-            torch._foreach_copy_(dst, src)
+            if self.cuda:   # one multi-tensor copy kernel
+                kernels.copy_mt(kernels.CopyList(dst, src))
+            else:
+                torch._foreach_copy_(dst, src)
         for p, g in zip(b.params, [p.value.grad for p in b.params]):
             if g is not None and self.cuda:
                 g.record_stream(torch.cuda.current_stream())   # freed after this stream's copy

@@ -123,6 +123,30 @@ def dp_step_peer(pb: PeerBucket, hp: nat.OfHparams, grad_scale, flags: int, stre
         nat.check(st, "of_dp_step_peer")
 
 
+class CopyList:
+    """Fixed (dst, src) tensor pairs for ``of_copy_mt`` (pointers captured once)."""
+
+    __slots__ = ("n", "dst", "src", "nbytes", "keep")
+
+    def __init__(self, dsts, srcs):
+        if len(dsts) != len(srcs):
+            raise ConfigError("copy list: dst and src lengths differ")
+        self.n = len(dsts)
+        self.dst = (ctypes.c_void_p * max(self.n, 1))(*[d.data_ptr() for d in dsts])
+        self.src = (ctypes.c_void_p * max(self.n, 1))(*[s.data_ptr() for s in srcs])
+        self.nbytes = (ctypes.c_int64 * max(self.n, 1))(*[d.numel() * d.element_size() for d in dsts])
+        for d, s in zip(dsts, srcs):
+            if d.numel() * d.element_size() != s.numel() * s.element_size() or d.stride() != s.stride():
+                raise ConfigError("copy list: a pair differs in size or layout")
+        self.keep = (list(dsts), list(srcs))
+
+
+def copy_mt(cl: CopyList, stream=None) -> None:
+    st = nat.lib().of_copy_mt(ctypes.cast(cl.dst, nat._PP), ctypes.cast(cl.src, nat._PP),
+                              cl.nbytes, cl.n, _handle(stream))
+    nat.check(st, "of_copy_mt")
+
+
 def sqnorm(tl: TensorList, workspace: torch.Tensor, out: torch.Tensor, accumulate: bool,
            stream) -> None:
     st = nat.lib().of_sqnorm_mt(tl.ref, workspace.data_ptr(), workspace.numel(), out.data_ptr(),

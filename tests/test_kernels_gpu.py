@@ -354,3 +354,24 @@ def test_peer_step_simulated_ranks_on_one_gpu(world, kind, mixed):
         for k, name in enumerate(names):
             got = states[r][k].cpu().numpy()
             assert got.tobytes() == slots[name][r * S:(r + 1) * S].tobytes(), (r, name)
+
+
+def test_copy_mt_many_tensors_any_alignment():
+    """of_copy_mt: >256 tensors (two launches), odd byte counts and unaligned views."""
+    torch.manual_seed(0)
+    base = torch.randn(100000, device=DEV)
+    srcs, dsts = [], []
+    off = 1
+    for i in range(300):
+        n = int(torch.randint(1, 200, (1,)))
+        srcs.append(base[off:off + n])            # 4-byte aligned only for most
+        dsts.append(torch.empty(n, device=DEV))
+        off += n + 1
+    srcs.append(torch.randn(12345, device=DEV, dtype=torch.float64))
+    dsts.append(torch.empty(12345, device=DEV, dtype=torch.float64))
+    srcs.append(torch.randn(7, device=DEV).to(torch.bfloat16))
+    dsts.append(torch.empty(7, device=DEV, dtype=torch.bfloat16))
+    kernels.copy_mt(kernels.CopyList(dsts, srcs))
+    torch.cuda.synchronize()
+    for d, s in zip(dsts, srcs):
+        assert torch.equal(d, s)
