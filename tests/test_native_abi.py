@@ -99,6 +99,12 @@ def test_invalid_arguments_rejected_before_launch():
     assert so.of_dp_step_peer(pb.ref, ctypes.byref(sgdm), None, 0, None) == nat.OF_ERR_INVALID
     assert so.of_dp_step_peer(pb.ref, ctypes.byref(sgdm), None, nat.OF_FLAG_ZERO_GRAD,
                               None) == nat.OF_ERR_INVALID
+    assert so.of_copy_mt(None, None, None, 3, None) == nat.OF_ERR_INVALID
+    nb = (ctypes.c_int64 * 1)(-4)
+    one = (ctypes.c_void_p * 1)(0x10)
+    assert so.of_copy_mt(ctypes.cast(one, nat._PP), ctypes.cast(one, nat._PP), nb, 1,
+                         None) == nat.OF_ERR_INVALID
+    assert so.of_copy_mt(None, None, None, 0, None) == nat.OF_OK
     assert so.of_exact_matmul(None, 0x10, 0x20, 2, 2, 2, nat.OF_F32, None) == nat.OF_ERR_INVALID
     assert so.of_exact_matmul(0x10, 0x10, 0x20, 70000, 2, 2, nat.OF_F32, None) == nat.OF_ERR_INVALID
     assert so.of_exact_matmul(0x10, 0x10, 0x20, 2, 2, 2, nat.OF_BF16, None) == nat.OF_ERR_UNSUPPORTED
