@@ -268,8 +268,13 @@ class DataParallelFusion:
             dst.append(view)
             src.append(g)
         if src:
-            if self.cuda:   # one multi-tensor copy kernel
-                kernels.copy_mt(kernels.CopyList(dst, src))
+            if self.cuda:   # one multi-tensor copy kernel (a gradient in another layout: copy_)
+                pairs = [(d, s) for d, s in zip(dst, src) if kernels.same_layout(d, s)]
+                for d, s in zip(dst, src):
+                    if not kernels.same_layout(d, s):
+                        d.copy_(s)
+                if pairs:
+                    kernels.copy_mt(kernels.CopyList([d for d, _ in pairs], [s for _, s in pairs]))
             else:
                 torch._foreach_copy_(dst, src)
         for p, g in zip(b.params, [p.value.grad for p in b.params]):

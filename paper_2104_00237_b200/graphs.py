@@ -101,7 +101,12 @@ class CapturedStep:
                     raise StateError("forward fusion left a parameter without a gradient")
                 # one multi-tensor copy kernel (torch's foreach copy costs ~10x
                 # more on MobileNetV2's 158 small tensors)
-                kernels.copy_mt(kernels.CopyList(self._ff_prev, cur))
+                same = [(d, c) for d, c in zip(self._ff_prev, cur) if kernels.same_layout(d, c)]
+                for d, c in zip(self._ff_prev, cur):
+                    if not kernels.same_layout(d, c):
+                        d.copy_(c)
+                if same:
+                    kernels.copy_mt(kernels.CopyList([d for d, _ in same], [c for _, c in same]))
         # liboptfuse_b200 kernel nodes in the graph (each replay launches them all)
         self.native_launches = _native.launch_count() - n0
         if self.dstep is not None:

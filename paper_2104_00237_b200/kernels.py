@@ -136,9 +136,20 @@ class CopyList:
         self.src = (ctypes.c_void_p * max(self.n, 1))(*[s.data_ptr() for s in srcs])
         self.nbytes = (ctypes.c_int64 * max(self.n, 1))(*[d.numel() * d.element_size() for d in dsts])
         for d, s in zip(dsts, srcs):
-            if d.numel() * d.element_size() != s.numel() * s.element_size() or d.stride() != s.stride():
+            if not same_layout(d, s):
                 raise ConfigError("copy list: a pair differs in size or layout")
         self.keep = (list(dsts), list(srcs))
+
+
+def same_layout(a, b) -> bool:
+    """Same dtype, shape and element order in memory (strides of size-1
+    dimensions are arbitrary), both dense: a byte copy moves a into b."""
+    if a.dtype != b.dtype or a.shape != b.shape:
+        return False
+    if any(sa != sb for n, sa, sb in zip(a.shape, a.stride(), b.stride()) if n > 1):
+        return False
+    from torch._prims_common import is_non_overlapping_and_dense
+    return is_non_overlapping_and_dense(a) and is_non_overlapping_and_dense(b)
 
 
 def copy_mt(cl: CopyList, stream=None) -> None:
