@@ -211,3 +211,15 @@ def test_checkpoint_rejects_foreign_or_mismatched_state():
           "master": {}}
     with pytest.raises(errors.ConfigError, match="checkpoint is for"):
         checkpoint.load_state_dict(g, pol, sd)
+
+
+def test_same_layout_ignores_strides_of_size_one_dims():
+    from paper_2104_00237_b200.kernels import same_layout
+    w = torch.empty(16, 32, 1, 1).contiguous(memory_format=torch.channels_last)
+    g = torch.empty(16, 32, 1, 1)
+    assert w.stride() != g.stride() and same_layout(w, g)
+    a = torch.empty(4, 3, 3, 3).contiguous(memory_format=torch.channels_last)
+    b = torch.empty(4, 3, 3, 3)
+    assert not same_layout(a, b)
+    assert not same_layout(torch.empty(4), torch.empty(4, dtype=torch.float64))
+    assert not same_layout(torch.empty(8)[::2], torch.empty(4))
