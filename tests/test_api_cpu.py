@@ -215,8 +215,8 @@ def test_checkpoint_rejects_foreign_or_mismatched_state():
 
 def test_same_layout_ignores_strides_of_size_one_dims():
     from paper_2104_00237_b200.kernels import same_layout
-    w = torch.empty(16, 32, 1, 1).contiguous(memory_format=torch.channels_last)
-    g = torch.empty(16, 32, 1, 1)
+    w = torch.empty(16, 32, 1, 1)
+    g = torch.empty_strided((16, 32, 1, 1), (32, 1, 32, 32))   # channels-last strides
     assert w.stride() != g.stride() and same_layout(w, g)
     a = torch.empty(4, 3, 3, 3).contiguous(memory_format=torch.channels_last)
     b = torch.empty(4, 3, 3, 3)
