@@ -526,7 +526,7 @@ def _dense(t) -> bool:
     span in some stride order (contiguous, channels-last, ...)."""
     if t.is_contiguous() or t.is_contiguous(memory_format=torch.channels_last):
         return True
-    from torch._prims_common import is_non_overlapping_and_dense
+    from torch._prims_common import is_non_overlapping_and_dense_or_false as is_non_overlapping_and_dense
     return is_non_overlapping_and_dense(t)
 
 

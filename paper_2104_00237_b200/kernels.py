@@ -148,7 +148,7 @@ def same_layout(a, b) -> bool:
         return False
     if any(sa != sb for n, sa, sb in zip(a.shape, a.stride(), b.stride()) if n > 1):
         return False
-    from torch._prims_common import is_non_overlapping_and_dense
+    from torch._prims_common import is_non_overlapping_and_dense_or_false as is_non_overlapping_and_dense
     return is_non_overlapping_and_dense(a) and is_non_overlapping_and_dense(b)
 
 
