@@ -269,12 +269,14 @@ class DataParallelFusion:
             src.append(g)
         if src:
             if self.cuda:   # one multi-tensor copy kernel (a gradient in another layout: copy_)
-                pairs = [(d, s) for d, s in zip(dst, src) if kernels.same_layout(d, s)]
-                for d, s in zip(dst, src):
-                    if not kernels.same_layout(d, s):
+                ok = [kernels.same_layout(d, s) for d, s in zip(dst, src)]
+                for d, s, k in zip(dst, src, ok):
+                    if not k:
                         d.copy_(s)
-                if pairs:
-                    kernels.copy_mt(kernels.CopyList([d for d, _ in pairs], [s for _, s in pairs]))
+                pd = [d for d, k in zip(dst, ok) if k]
+                if pd:
+                    ps = [s for s, k in zip(src, ok) if k]
+                    kernels.copy_mt(kernels.CopyList(pd, ps, checked=True))
             else:
                 torch._foreach_copy_(dst, src)
         for p, g in zip(b.params, [p.value.grad for p in b.params]):
@@ -524,10 +526,7 @@ class DataParallelFusion:
 def _dense(t) -> bool:
     """Non-overlapping and dense: the elements fill [0, numel) of its storage
     span in some stride order (contiguous, channels-last, ...)."""
-    if t.is_contiguous() or t.is_contiguous(memory_format=torch.channels_last):
-        return True
-    from torch._prims_common import is_non_overlapping_and_dense_or_false as is_non_overlapping_and_dense
-    return is_non_overlapping_and_dense(t)
+    return kernels.is_dense(t)
 
 
 class _NullCtx:

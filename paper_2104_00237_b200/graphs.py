@@ -101,12 +101,14 @@ class CapturedStep:
                     raise StateError("forward fusion left a parameter without a gradient")
                 # one multi-tensor copy kernel (torch's foreach copy costs ~10x
                 # more on MobileNetV2's 158 small tensors)
-                same = [(d, c) for d, c in zip(self._ff_prev, cur) if kernels.same_layout(d, c)]
-                for d, c in zip(self._ff_prev, cur):
-                    if not kernels.same_layout(d, c):
+                ok = [kernels.same_layout(d, c) for d, c in zip(self._ff_prev, cur)]
+                for d, c, k in zip(self._ff_prev, cur, ok):
+                    if not k:
                         d.copy_(c)
+                same = [(d, c) for d, c, k in zip(self._ff_prev, cur, ok) if k]
                 if same:
-                    kernels.copy_mt(kernels.CopyList([d for d, _ in same], [c for _, c in same]))
+                    kernels.copy_mt(kernels.CopyList([d for d, _ in same], [c for _, c in same],
+                                                     checked=True))
         # liboptfuse_b200 kernel nodes in the graph (each replay launches them all)
         self.native_launches = _native.launch_count() - n0
         if self.dstep is not None:

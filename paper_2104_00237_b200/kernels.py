@@ -128,16 +128,17 @@ class CopyList:
 
     __slots__ = ("n", "dst", "src", "nbytes", "keep")
 
-    def __init__(self, dsts, srcs):
+    def __init__(self, dsts, srcs, checked: bool = False):
         if len(dsts) != len(srcs):
             raise ConfigError("copy list: dst and src lengths differ")
         self.n = len(dsts)
         self.dst = (ctypes.c_void_p * max(self.n, 1))(*[d.data_ptr() for d in dsts])
         self.src = (ctypes.c_void_p * max(self.n, 1))(*[s.data_ptr() for s in srcs])
         self.nbytes = (ctypes.c_int64 * max(self.n, 1))(*[d.numel() * d.element_size() for d in dsts])
-        for d, s in zip(dsts, srcs):
-            if not same_layout(d, s):
-                raise ConfigError("copy list: a pair differs in size or layout")
+        if not checked:
+            for d, s in zip(dsts, srcs):
+                if not same_layout(d, s):
+                    raise ConfigError("copy list: a pair differs in size or layout")
         self.keep = (list(dsts), list(srcs))
 
 
@@ -148,8 +149,19 @@ def same_layout(a, b) -> bool:
         return False
     if any(sa != sb for n, sa, sb in zip(a.shape, a.stride(), b.stride()) if n > 1):
         return False
-    from torch._prims_common import is_non_overlapping_and_dense_or_false as is_non_overlapping_and_dense
-    return is_non_overlapping_and_dense(a) and is_non_overlapping_and_dense(b)
+    return is_dense(a) and is_dense(b)
+
+
+def is_dense(t) -> bool:
+    """Non-overlapping and dense: the dimensions of size > 1, ordered by
+    stride, tile [0, numel) exactly (contiguous, channels-last, any permutation)."""
+    dims = sorted((st, n) for n, st in zip(t.shape, t.stride()) if n > 1)
+    expect = 1
+    for st, n in dims:
+        if st != expect:
+            return False
+        expect *= n
+    return True
 
 
 def copy_mt(cl: CopyList, stream=None) -> None:
