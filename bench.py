@@ -81,6 +81,9 @@ def parse_args(argv=None):
     ap.add_argument("--dp-graphs", type=int, default=1,
                     help="1: capture data-parallel iterations (NCCL collectives included) as CUDA "
                          "graphs too (0: eager data parallel)")
+    ap.add_argument("--dp-transport", default="nccl", choices=("nccl", "peer"),
+                    help="data parallel: NCCL reduce-scatter/all-gather around the sharded kernel, "
+                         "or the fused peer-memory kernel over torch symmetric memory")
     ap.add_argument("--force-dp", action="store_true",
                     help="run the data-parallel code path (NCCL process group, DataParallelFusion, "
                          "DDP baselines) even at one GPU: the N>1 path's smoke test")
@@ -332,7 +335,8 @@ def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
             g.use_master_weights()
             x = x.to(torch.bfloat16) if x.is_floating_point() else x
         pol = of.OptimizerPolicy(wl["kind"], **wl["hp"])
-        dpf = DataParallelFusion(g, pol, bucket_elems=bucket_elems or args.bucket_elems)
+        dpf = DataParallelFusion(g, pol, bucket_elems=bucket_elems or args.bucket_elems,
+                                 transport=getattr(args, "dp_transport", "nccl"))
         dp_run = {"baseline": dpf.run_baseline, "forward-fusion": dpf.run_forward_fusion,
                   "backward-fusion": dpf.run_backward_fusion}[schedule]
         graphed = graphed and bool(args.dp_graphs)   # NCCL collectives captured in the graph
@@ -695,9 +699,11 @@ def run_ours(args) -> dict:
                       "cuda_graph": bool(args.graphs) and (not args.dp or bool(args.dp_graphs)),
                       "channels_last": bool(args.channels_last),
                       "parallelism": f"dp{dist.world}",
-                      "dp_path": ("sharded fused update: per-bucket NCCL reduce-scatter -> update "
-                                  "-> all-gather; unfused baseline DDP + torch.optim"
-                                  if args.dp else None),
+                      "dp_path": (("sharded fused update: per-bucket NCCL reduce-scatter -> update "
+                                   "-> all-gather" if args.dp_transport == "nccl" else
+                                   "fused peer-memory kernel per bucket (reduce-scatter + update + "
+                                   "all-gather in one kernel over symmetric memory)")
+                                  + "; unfused baseline DDP + torch.optim" if args.dp else None),
                       "l2": "256 MiB buffer zeroed before every timed step (inside the timed region)",
                       "model_math": ("fp32 parameters/activations; TF32 tensor cores for convolutions "
                                      f"(cudnn.allow_tf32={torch.backends.cudnn.allow_tf32}) and matmuls "
