@@ -190,7 +190,7 @@ int of_copy_mt(void* const* dst, const void* const* src, const int64_t* nbytes, 
 
 /* Parity-harness helper (not on the update path): out[M][N] = a[M][K] @ b[K][N]
  * (row-major, contiguous) with the reference engine's fixed accumulation order
- * (tensor.py: out = 0; out = out + a[:, k] * b[k, :] for k ascending, every
+ * (tensor.py:91-105 matmul_arrays: out = 0; out += a[:, k] * b[k, :] for k ascending, every
  * product and sum correctly rounded), so the synthetic graphs' gradients are
  * bit-identical to the reference's.  dtype: OF_F32 or OF_F64; M <= 65535. */
 int of_exact_matmul(const void* a, const void* b, void* out, int64_t M, int64_t K, int64_t N,

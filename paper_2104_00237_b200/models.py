@@ -44,7 +44,7 @@ def seeded_uniform(shape, lo: float, hi: float, seed: int, precision: str = "f32
 
 def fixed_order_matmul(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
     """a @ b accumulated one rank-1 product per contraction index, ascending,
-    each product and sum a separately rounded IEEE operation (tensor.py's
+    each product and sum a separately rounded IEEE operation (tensor.py:91-105
     order).  On the GPU one kernel (``of_exact_matmul``) computes it; the host
     loop serves the CPU-side tests of the synthetic graphs."""
     if a.is_cuda and a.dtype in (torch.float32, torch.float64) and a.shape[0] <= 65535:
