@@ -25,6 +25,8 @@
 // them alive in `hold_` until the update stream has been joined.
 #include <torch/extension.h>
 #include <ATen/cuda/CUDAContext.h>
+#include <c10/cuda/CUDACachingAllocator.h>
+#include <c10/cuda/CUDAGuard.h>
 #include <torch/csrc/autograd/function_hook.h>
 #include <torch/csrc/autograd/variable.h>
 
@@ -220,6 +222,7 @@ class Engine : public std::enable_shared_from_this<Engine> {
       // readiness only: the group callback (data-parallel buckets) runs once
       // per complete group instead of Python once per parameter
       if (group_cb_ && ++ready_[gi] == static_cast<int>(groups_[gi].members.size())) {
+        if (gi < static_cast<int>(views_.size()) && !views_[gi].empty()) gather_group(gi);
         py::gil_scoped_acquire gil;
         group_cb_(gi);
       }
@@ -229,6 +232,70 @@ class Engine : public std::enable_shared_from_this<Engine> {
   }
 
   void set_group_callback(py::object cb) { group_cb_ = cb.is_none() ? py::object() : cb; }
+
+  // Data parallel: where group gi's gradients land (views into its flat
+  // buffer, one per member, same strides as the parameter).  When the group
+  // completes, its gradients are copied there on the side (communication)
+  // stream with one of_copy_mt launch and released, before the Python
+  // callback issues the collectives -- no Python per parameter.
+  void set_group_views(int gi, std::vector<at::Tensor> views) {
+    if (gi < 0 || gi >= static_cast<int>(groups_.size()))
+      throw std::out_of_range("optfuse: group index out of range");
+    if (views.size() != groups_[gi].members.size())
+      throw std::invalid_argument("optfuse: one view per group member");
+    if (views_.size() < groups_.size()) views_.resize(groups_.size());
+    views_[gi] = std::move(views);
+  }
+
+  static bool same_layout(const at::Tensor& a, const at::Tensor& b) {
+    if (a.scalar_type() != b.scalar_type() || a.sizes() != b.sizes()) return false;
+    for (int64_t d = 0; d < a.dim(); ++d)
+      if (a.size(d) > 1 && a.stride(d) != b.stride(d)) return false;
+    return a.is_non_overlapping_and_dense() && b.is_non_overlapping_and_dense();
+  }
+
+  void gather_group(int gi) {
+    Group& G = groups_[gi];
+    cudaStream_t cur = current();
+    cudaStream_t s = side_ ? side_ : cur;
+    if (side_) {
+      cuda_check(cudaEventRecord(G.ready, cur), "cudaEventRecord");
+      cuda_check(cudaStreamWaitEvent(side_, G.ready, 0), "cudaStreamWaitEvent");
+    }
+    const auto dev = params_[G.members[0]].device();
+    c10::cuda::CUDAStream cs = c10::cuda::getStreamFromExternal(s, dev.index());
+    c10::cuda::CUDAStreamGuard guard(cs);
+    std::vector<void*> dst;
+    std::vector<const void*> src;
+    std::vector<int64_t> nbytes;
+    std::vector<at::Tensor> used;
+    const auto& views = views_[gi];
+    for (size_t k = 0; k < G.members.size(); ++k) {
+      at::Tensor& gr = params_[G.members[k]].mutable_grad();
+      const at::Tensor& v = views[k];
+      if (!gr.defined()) {          // no contribution this iteration: the reference steps with 0
+        v.zero_();
+        continue;
+      }
+      if (same_layout(v, gr)) {
+        dst.push_back(v.data_ptr());
+        src.push_back(gr.data_ptr());
+        nbytes.push_back(v.numel() * static_cast<int64_t>(v.element_size()));
+      } else {
+        v.copy_(gr);
+      }
+      used.push_back(gr);
+      gr = at::Tensor();
+    }
+    if (!dst.empty()) {
+      const int st = of_copy_mt(dst.data(), src.data(), nbytes.data(), static_cast<int>(dst.size()), s);
+      if (st != OF_OK)
+        throw std::runtime_error(std::string("of_copy_mt: ") + of_status_string(st) + " (" +
+                                 of_last_error() + ")");
+    }
+    // released on the compute stream's allocator, used on s: reuse waits for s
+    for (auto& g : used) c10::cuda::CUDACachingAllocator::recordStream(g.storage().data_ptr(), cs);
+  }
 
   // Launch every group that did not complete during backward (parameters
   // that received no gradient this iteration still step, with g = 0, as the
@@ -525,6 +592,7 @@ class Engine : public std::enable_shared_from_this<Engine> {
   std::vector<ProfRec> prof_;
   int64_t launches_ = 0;
   py::object callback_, group_cb_;
+  std::vector<std::vector<at::Tensor>> views_;
 };
 
 void FusionHook::operator()(const Variable&) {
@@ -545,6 +613,7 @@ PYBIND11_MODULE(_optfuse_engine, m) {
       .def("remove_hooks", &Engine::remove_hooks)
       .def("set_callback", &Engine::set_callback)
       .def("set_group_callback", &Engine::set_group_callback)
+      .def("set_group_views", &Engine::set_group_views)
       .def("bf_begin", &Engine::bf_begin, py::arg("launch") = true)
       .def("disarm", &Engine::disarm)
       .def("bf_finish", &Engine::bf_finish)

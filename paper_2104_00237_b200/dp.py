@@ -50,7 +50,8 @@ TRANSPORTS = ("nccl", "peer")
 
 class _Bucket:
     __slots__ = ("index", "params", "offsets", "flat_param", "flat_grad", "grad_shard", "slots",
-                 "shard", "master", "tl", "peer", "hparam", "hgrad", "sq_tl", "grad_views", "ready",
+                 "shard", "master", "tl", "peer", "hparam", "hgrad", "sq_tl", "grad_views", "gathered",
+                 "ready",
                  "event", "done", "leader", "pending")
 
     def __init__(self, index):
@@ -177,6 +178,7 @@ class DataParallelFusion:
                 b.done = torch.cuda.Event()
             b.ready = 0
             b.pending = False
+            b.gathered = False
             self.buckets.append(b)
         if self.mixed:
             for p in graph.parameters:
@@ -254,6 +256,12 @@ class DataParallelFusion:
     # -- the per-bucket pipeline ----------------------------------------------
 
     def _gather_grads(self, b) -> None:
+        if b.gathered:
+            b.gathered = False
+            return
+        self._gather_grads_host(b)
+
+    def _gather_grads_host(self, b) -> None:
         """Copy the bucket's gradients into flat_grad with one multi-tensor copy
         and release them.  AccumulateGrad steals each incoming gradient
         (``p.grad`` is None), where persistent views into flat_grad would cost
@@ -345,7 +353,11 @@ class DataParallelFusion:
             g = self.graph
             eng = native_engine_module().Engine(
                 [p.value for p in g.parameters], [[p.id for p in b.params] for b in self.buckets],
-                [[p.id for p in L.params] for L in g.layers], 0)
+                [[p.id for p in L.params] for L in g.layers], self.comm.cuda_stream)
+            # the engine gathers each completed bucket's gradients into flat_grad
+            # on the communication stream (one of_copy_mt), then calls back
+            for gi, b in enumerate(self.buckets):
+                eng.set_group_views(gi, b.grad_views)
             eng.set_group_callback(self._on_bucket_ready)
             eng.install_hooks()
             g._hook_owner = eng
@@ -363,6 +375,7 @@ class DataParallelFusion:
         if self._mode is None:
             return
         b.ready = len(b.params)
+        b.gathered = True       # the engine already copied the gradients into flat_grad
         self._bucket_ready(b)
 
     def _backward(self) -> None:
