@@ -55,7 +55,8 @@ class StepReport:
     def __init__(self, schedule: str, loss, trace, events=None, fused: bool = False,
                  pending_updates: int = 0):
         self.schedule = schedule
-        self.loss = loss
+        # the iteration's backward has run: the caller gets a plain device value
+        self.loss = loss.detach() if isinstance(loss, torch.Tensor) else loss
         self.trace = trace
         self.pending_updates = pending_updates
         self._events = events
