@@ -784,6 +784,8 @@ def run_ours(args) -> dict:
         if dist.rank == 0 and dist.world == 1:
             res["cpu_baseline"] = cpu_baseline(args, args.cpu_iters)
             res["cpu_update_baseline"] = cpu_update_baseline(std)
+            from oracle import timing
+            res["cpu_harness_baseline"] = dict(timing.reference_harness_breakdown(), kind="port")
     res["clocks"] = clocks
     dist.close()
     return res

@@ -80,3 +80,27 @@ def reference_update_rate(kind: str, hp: dict, elems: int = 1 << 22, reps: int =
     bpe = 4 * (2 + 2 * len(optim_ref.SLOTS[kind])) + 4
     return {"elems_per_s": elems / sec, "gbs": elems * bpe / sec / 1e9, "threads": 1,
             "sample": f"{reps} steps of one {elems}-element f32 tensor"}
+
+
+def reference_harness_breakdown(layers: int = 8, width: int = 32, batch: int = 32, iters: int = 30,
+                                warmup: int = 5) -> dict:
+    """The reference CLI's default workload (chain 8x32, adam 1e-3, batch 32)
+    through the oracle port of its three schedules, numpy single-threaded as
+    the reference runs: mean ms per iteration of each (the CPU side of the
+    harness breakdown the GPU CLI reports)."""
+    from . import chain_ref
+    out = {}
+    for name, run in (("baseline", chain_ref.run_baseline),
+                      ("forward-fusion", chain_ref.run_forward_fusion),
+                      ("backward-fusion", chain_ref.run_backward_fusion)):
+        m = chain_ref.build("chain", layers=layers, width=width, seed=0)
+        pol = chain_ref.Policy("adam", eta=1e-3)
+        xs = chain_ref.iteration_inputs(m, batch, 0, warmup + iters)
+        for x in xs[:warmup]:
+            run(m, pol, x)
+        t0 = time.perf_counter()
+        for x in xs[warmup:]:
+            run(m, pol, x)
+        out[name] = (time.perf_counter() - t0) / iters * 1e3
+    return {"ms_per_iter": {k: round(v, 3) for k, v in out.items()}, "threads": 1,
+            "sample": f"chain {layers}x{width}, adam, batch {batch}, {iters} iterations each"}
