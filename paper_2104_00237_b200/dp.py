@@ -535,6 +535,53 @@ class DataParallelFusion:
         self._apply_deferred()
         return n
 
+    # -- checkpoint / resume ---------------------------------------------------
+
+    def state_dict(self) -> dict:
+        """This rank's training state: pending updates applied first, then the
+        module tensors (identical on every rank after the all-gather), the
+        policy and, per bucket, the history (and fp32 master) of the shard this
+        rank owns.  Each rank saves its own; resume with the same world size
+        and buckets."""
+        from .checkpoint import _POLICY_FIELDS
+        self.flush()
+        with torch.no_grad():
+            return {"format": "optfuse-b200-dp/1", "world": self.world, "rank": self.rank,
+                    "buckets": [{"shard": (b.shard.start, b.shard.stop),
+                                 "slots": {k: v.detach().clone() for k, v in b.slots.items()},
+                                 "master": b.master.detach().clone() if b.master is not None else None}
+                                for b in self.buckets],
+                    "model": {k: v.detach().clone() for k, v in self.graph.module.state_dict().items()},
+                    "policy": {f: getattr(self.policy, f) for f in _POLICY_FIELDS},
+                    "pending_t": getattr(self, "_pending_t", None)}
+
+    def load_state_dict(self, sd: dict) -> None:
+        from .checkpoint import _POLICY_FIELDS
+        if sd.get("format") != "optfuse-b200-dp/1":
+            raise ConfigError("not an optfuse-b200 data-parallel checkpoint")
+        if sd["world"] != self.world or sd["rank"] != self.rank:
+            raise ConfigError(f"checkpoint of rank {sd['rank']}/{sd['world']}, this is "
+                              f"{self.rank}/{self.world}")
+        if len(sd["buckets"]) != len(self.buckets) or any(
+                tuple(bs["shard"]) != (b.shard.start, b.shard.stop)
+                for bs, b in zip(sd["buckets"], self.buckets)):
+            raise ConfigError("checkpoint buckets differ from this model's")
+        if sd["policy"]["kind"] != self.policy.kind:
+            raise ConfigError(f"checkpoint is for {sd['policy']['kind']!r}, policy is {self.policy.kind!r}")
+        if any(b.pending for b in self.buckets):
+            raise StateError("flush pending updates before loading a checkpoint")
+        for f in _POLICY_FIELDS:
+            setattr(self.policy, f, sd["policy"][f])
+        with torch.no_grad():
+            # module tensors land in the flat buffers the parameters view
+            self.graph.module.load_state_dict(sd["model"])
+            for bs, b in zip(sd["buckets"], self.buckets):
+                for k, v in bs["slots"].items():
+                    b.slots[k].copy_(v)
+                if b.master is not None:
+                    b.master.copy_(bs["master"])
+        self._pending_t = sd.get("pending_t")
+
 
 def _dense(t) -> bool:
     """Non-overlapping and dense: the elements fill [0, numel) of its storage
