@@ -212,6 +212,17 @@ class DataParallelFusion:
         self._leader_handles = None
         self.join_event = torch.cuda.Event() if self.cuda else None
 
+    @property
+    def _pending_t(self):
+        """Step index frozen when forward fusion deferred the updates
+        (schedule.py:133); kept on the Graph, where a CUDA-graph replay
+        (CapturedStep) advances it."""
+        return self.graph.pending_step_t
+
+    @_pending_t.setter
+    def _pending_t(self, t) -> None:
+        self.graph.pending_step_t = t
+
     def _symmetric(self, n: int, dt):
         """A zeroed flat buffer in torch symmetric memory and its handle (the
         peers' mappings of it: ``buffer_ptrs``; cross-rank ``barrier``)."""
@@ -502,7 +513,7 @@ class DataParallelFusion:
     def _leader(self, k: int):
         bs = self._fwd_buckets
         b = bs[k]
-        t = getattr(self, "_pending_t", None)
+        t = self._pending_t
         # a bucket made pending by the previous backward needs no wait: that
         # backward ended with the compute stream joining the communication
         # stream (and an event recorded then may predate a CUDA-graph capture)
@@ -524,7 +535,7 @@ class DataParallelFusion:
                 b.done.record(torch.cuda.current_stream())
 
     def _apply_deferred(self) -> None:
-        t = getattr(self, "_pending_t", None)
+        t = self._pending_t
         for b in self.buckets:
             if b.pending:   # (ordered after its reduce-scatter by the backward's join)
                 self._update_and_gather(b, t)
@@ -553,7 +564,7 @@ class DataParallelFusion:
                                 for b in self.buckets],
                     "model": {k: v.detach().clone() for k, v in self.graph.module.state_dict().items()},
                     "policy": {f: getattr(self.policy, f) for f in _POLICY_FIELDS},
-                    "pending_t": getattr(self, "_pending_t", None)}
+                    "pending_t": self._pending_t}
 
     def load_state_dict(self, sd: dict) -> None:
         from .checkpoint import _POLICY_FIELDS
