@@ -4,7 +4,7 @@ set -e
 cd "$(dirname "$0")/.."
 rm -f build/variants/*.so
 mkdir -p build/variants
-for v in "4 1 2 4 0" "4 1 2 4 1" "4 1 2 3 0" "4 1 4 2 0" "8 1 2 4 0" "4 1 1 8 0"; do
+for v in ${VARIANTS:-"4 1 2 4 0" "4 1 2 3 0" "4 1 4 2 0" "4 1 1 8 0" "4 1 4 3 0" "4 2 2 4 0" "8 1 4 2 0"}; do
   set -- $v
   /usr/local/cuda/bin/nvcc -O3 -gencode arch=compute_100a,code=sm_100a -lineinfo --fmad=false -std=c++17 \
     -Xcompiler -fPIC -shared -I include -DOF_UNROLL=$1 -DOF_MIN_BLOCKS=$2 -DOF_UNROLL_BF16=$3 \
