@@ -627,6 +627,14 @@ PYBIND11_MODULE(_optfuse_engine, m) {
       .def("num_pending", &Engine::num_pending)
       .def("ff_layer", &Engine::ff_layer)
       .def("ff_unit_lookahead", &Engine::ff_unit_lookahead, py::arg("u"), py::arg("depth") = 1)
+      // forward pre-hooks without a Python frame: functools.partial(engine.ff_hook, u, depth)
+      // is called by torch as hook(module, args) and returns None
+      .def("ff_hook",
+           [](Engine& e, int u, int depth, py::object, py::object) {
+             if (depth > 0) e.ff_unit_lookahead(u, depth);
+             else e.ff_layer(u);
+             return py::none();
+           })
       .def("ff_join", &Engine::ff_join)
       .def("set_ff_units", &Engine::set_ff_units)
       .def("reset_ff_units", &Engine::reset_ff_units)

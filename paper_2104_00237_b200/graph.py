@@ -244,6 +244,8 @@ class Graph:
             self._leader_handles = None
         if leaders:
             def make(fn):
+                if getattr(fn, "is_hook", False):   # already hook(module, args) -> None
+                    return fn
                 def hook(module, args):
                     fn()
                     return None  # a non-None return would replace the layer's input

@@ -27,6 +27,8 @@ per-parameter arithmetic, only the issue point of each update moves).
 
 from __future__ import annotations
 
+import functools
+
 import torch
 
 from . import checkpoint
@@ -305,8 +307,11 @@ def run_forward_fusion(graph: Graph, policy: OptimizerPolicy, inp, *, timing: bo
             return _f(u, _d)
     else:
         ff_layer = native.ff_layer
-    if prefetch and bucket_elems == 0:
-        bucket_elems = 1   # lookahead follows the recorded execution order: one unit per layer
+    if bucket_elems == 0 and tc is None:
+        # after the first iteration, one unit per executed layer in execution
+        # order (a shared parameter belongs to the layer that uses it first):
+        # the per-layer schedule, with hooks that call the engine directly
+        bucket_elems = 1
     bucketed = bucket_elems > 0 and tc is None and graph.exec_order is not None
     if bucketed:
         if eng.ff_bucket_elems != bucket_elems or eng.ff_prefetch != depth:
@@ -314,7 +319,12 @@ def run_forward_fusion(graph: Graph, policy: OptimizerPolicy, inp, *, timing: bo
             native.set_ff_units(units)
             eng.ff_bucket_elems = bucket_elems
             eng.ff_prefetch = depth
-            eng.ff_leaders = [(L, (lambda i=i: ff_layer(i))) for i, L in enumerate(leaders)]
+            hooks = []
+            for i, L in enumerate(leaders):
+                h = functools.partial(native.ff_hook, i, depth)   # no Python frame per layer
+                h.is_hook = True
+                hooks.append((L, h))
+            eng.ff_leaders = hooks
         graph.set_leader_hooks(eng.ff_leaders)
         apply_pending = None
     else:
