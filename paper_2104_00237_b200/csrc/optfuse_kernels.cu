@@ -28,7 +28,9 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 namespace {
 
@@ -71,6 +73,15 @@ int check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(OF_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
   return OF_OK;
+}
+
+// OPTFUSE_TMA=1 selects the TMA-staged kernel for large fp32 launches (read once).
+bool use_tma() {
+  static const bool on = [] {
+    const char* e = std::getenv("OPTFUSE_TMA");
+    return e != nullptr && e[0] == '1';
+  }();
+  return on;
 }
 
 int sm_count() {
@@ -455,6 +466,176 @@ mt_step_kernel(const __grid_constant__ MTParams<CAP> mp, const Op op_in,
   }
 }
 
+// ---------------------------------------------------------------------------
+// TMA-staged variant (experimental, OPTFUSE_TMA=1): the input streams of each
+// 2048-element tile (theta, grad, history) arrive in shared memory by bulk
+// copies (cp.async.bulk, completion counted on an mbarrier) issued
+// kTmaStages tiles ahead by one thread; the block computes from shared memory
+// and stores the results straight to global memory.  One CTA per SM.  Tiles
+// that are not full or not 16-byte aligned are read from global memory
+// directly.  Same arithmetic, so the same bits.
+// ---------------------------------------------------------------------------
+constexpr int kTmaTile = 2048;
+constexpr int kTmaStages = 4;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+               :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+               " selp.u32 %0, 1, 0, p;\n}"
+               : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+template <class T, class G, int kSlots>
+struct TmaLayout {
+  static constexpr int kP = kTmaTile * sizeof(T);
+  static constexpr int kG = kTmaTile * sizeof(G);
+  static constexpr int kStage = kP + kG + kSlots * kP;
+};
+
+template <class Op, class T, class G, int CAP>
+__global__ void __launch_bounds__(kThreads, 1)
+mt_step_tma_kernel(const __grid_constant__ MTParams<CAP> mp, const Op op_in,
+                   const float* __restrict__ gscale, uint32_t flags, const StepSrc step) {
+  using GV = typename GradVal<G>::type;
+  using L = TmaLayout<T, G, Op::kSlots>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t full[kTmaStages];
+  Op op = op_in;
+  if (step.offset != nullptr) {
+    int64_t t = step.t_base + *step.offset;
+    t = t < 1 ? 1 : (t >= step.rows ? step.rows - 1 : t);
+    op.set_step(step.table[2 * t], step.table[2 * t + 1]);
+  }
+  const bool zero_grad = (flags & OF_FLAG_ZERO_GRAD) != 0;
+  const bool shadow = (flags & OF_FLAG_SHADOW_BF16) != 0;
+  const bool has_scale = gscale != nullptr;
+  const T scale = has_scale ? T(*gscale) : T(1);
+  const int total = mp.tile_end[mp.count - 1];
+  const int ntiles = total > static_cast<int>(blockIdx.x)
+                         ? (total - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1 : 0;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kTmaStages; ++st) mbar_init(&full[st], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  struct Where { int ti; int64_t base; int len; };
+  auto locate = [&](int k, int& hint) -> Where {
+    const int tile = static_cast<int>(blockIdx.x) + k * static_cast<int>(gridDim.x);
+    hint = find_tensor(mp, hint, tile);
+    const int tfirst = hint ? mp.tile_end[hint - 1] : 0;
+    const int64_t base = static_cast<int64_t>(tile - tfirst) * kTmaTile;
+    const int64_t rem = mp.n[hint] - base;
+    return Where{hint, base, rem < kTmaTile ? static_cast<int>(rem) : kTmaTile};
+  };
+  auto staged = [&](const Where& w) {
+    if (w.len != kTmaTile) return false;
+    const T* p = static_cast<const T*>(mp.p[w.ti]) + w.base;
+    const G* g = static_cast<const G*>(mp.g[w.ti]) + w.base;
+    if (!aligned(p, 16) || !aligned(g, 16)) return false;
+    if (Op::kSlots >= 1 && !aligned(static_cast<const T*>(mp.s0[w.ti]) + w.base, 16)) return false;
+    if (Op::kSlots >= 2 && !aligned(static_cast<const T*>(mp.s1[w.ti]) + w.base, 16)) return false;
+    if (shadow && !aligned(static_cast<const __nv_bfloat16*>(mp.sh[w.ti]) + w.base, 8)) return false;
+    return true;
+  };
+  int hint_p = 0;
+  auto issue = [&](int k) {                       // thread 0 only
+    const Where w = locate(k, hint_p);
+    uint64_t* bar = &full[k % kTmaStages];
+    unsigned char* st = smem + (k % kTmaStages) * L::kStage;
+    if (!staged(w)) { mbar_arrive(bar); return; }
+    mbar_arrive_expect_tx(bar, L::kStage);
+    bulk_g2s(st, static_cast<const T*>(mp.p[w.ti]) + w.base, L::kP, bar);
+    bulk_g2s(st + L::kP, static_cast<const G*>(mp.g[w.ti]) + w.base, L::kG, bar);
+    if (Op::kSlots >= 1)
+      bulk_g2s(st + L::kP + L::kG, static_cast<const T*>(mp.s0[w.ti]) + w.base, L::kP, bar);
+    if (Op::kSlots >= 2)
+      bulk_g2s(st + 2 * L::kP + L::kG, static_cast<const T*>(mp.s1[w.ti]) + w.base, L::kP, bar);
+  };
+  if (threadIdx.x == 0)
+    for (int k = 0; k < kTmaStages && k < ntiles; ++k) issue(k);
+
+  int hint_c = 0;
+  for (int k = 0; k < ntiles; ++k) {
+    const Where w = locate(k, hint_c);
+    const bool tma = staged(w);
+    uint64_t* bar = &full[k % kTmaStages];
+    unsigned char* st = smem + (k % kTmaStages) * L::kStage;
+    uint32_t tries = 0;
+    while (!mbar_try_wait(bar, (k / kTmaStages) & 1))
+      if (++tries > (1u << 24)) __trap();          // never hang the GPU on a lost transaction
+    T* p = static_cast<T*>(mp.p[w.ti]) + w.base;
+    G* g = static_cast<G*>(mp.g[w.ti]) + w.base;
+    T* s0 = Op::kSlots >= 1 ? static_cast<T*>(mp.s0[w.ti]) + w.base : nullptr;
+    T* s1 = Op::kSlots >= 2 ? static_cast<T*>(mp.s1[w.ti]) + w.base : nullptr;
+    __nv_bfloat16* sh = shadow ? static_cast<__nv_bfloat16*>(mp.sh[w.ti]) + w.base : nullptr;
+    if (tma) {
+      const T* sp = reinterpret_cast<const T*>(st);
+      const G* sg = reinterpret_cast<const G*>(st + L::kP);
+      const T* ss0 = reinterpret_cast<const T*>(st + L::kP + L::kG);
+      const T* ss1 = reinterpret_cast<const T*>(st + 2 * L::kP + L::kG);
+#pragma unroll
+      for (int u = 0; u < kTmaTile / (kThreads * kVec); ++u) {
+        const int j = threadIdx.x + u * kThreads;
+        T vp[4], v0[4], v1[4];
+        GV vg[4];
+        ld4(sp + 4 * j, vp);
+        ld4(sg + 4 * j, vg);
+        if (Op::kSlots >= 1) ld4(ss0 + 4 * j, v0);
+        if (Op::kSlots >= 2) ld4(ss1 + 4 * j, v1);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          T gk = static_cast<T>(vg[e]);
+          if (has_scale) gk = o_mul(gk, scale);
+          op(vp[e], gk, v0[e], v1[e]);
+        }
+        st4(p + 4 * j, vp);
+        if (Op::kSlots >= 1) st4(s0 + 4 * j, v0);
+        if (Op::kSlots >= 2) st4(s1 + 4 * j, v1);
+        if (zero_grad) st4_zero(g + 4 * j);
+        if (shadow) st4_bf16(sh + 4 * j, vp);
+      }
+    } else {
+      for (int e = threadIdx.x; e < w.len; e += kThreads) {
+        T pv = p[e];
+        T a = Op::kSlots >= 1 ? s0[e] : T(0);
+        T b = Op::kSlots >= 2 ? s1[e] : T(0);
+        T gk = static_cast<T>(ld1(g + e));
+        if (has_scale) gk = o_mul(gk, scale);
+        op(pv, gk, a, b);
+        p[e] = pv;
+        if (Op::kSlots >= 1) s0[e] = a;
+        if (Op::kSlots >= 2) s1[e] = b;
+        if (zero_grad) st1_zero(g + e);
+        if (shadow) sh[e] = __float2bfloat16_rn(static_cast<float>(pv));
+      }
+    }
+    __syncthreads();                                // every thread is done with this stage
+    if (threadIdx.x == 0 && k + kTmaStages < ntiles) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic reads before async writes
+      issue(k + kTmaStages);
+    }
+  }
+}
+
 // Sum of squares, per-CTA f64 partials (deterministic order within a CTA).
 template <class G, int CAP>
 __global__ void __launch_bounds__(kThreads)
@@ -633,6 +814,24 @@ int launch_step_chunk(const of_tensor_list* l, int first, int count, const Op& o
     return check_launch("mt_step_kernel");
   }
   if (tiles > INT32_MAX) return fail(OF_ERR_INVALID, "tensor list too large for one launch");
+  if constexpr (std::is_same<T, float>::value) {
+    if (use_tma() && max_ctas == 0) {
+      using L = TmaLayout<T, G, Op::kSlots>;
+      constexpr int smem = kTmaStages * L::kStage;
+      static bool configured = false;
+      if (!configured) {
+        if (cudaFuncSetAttribute(mt_step_tma_kernel<Op, T, G, CAP>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+          return fail(OF_ERR_CUDA, "cudaFuncSetAttribute(smem %d)", smem);
+        configured = true;
+      }
+      const int64_t ttiles = pack<CAP>(l, first, count, mp, kTmaTile);
+      const int64_t tcap = sm_count();
+      const int grid = static_cast<int>(ttiles < tcap ? ttiles : tcap);
+      mt_step_tma_kernel<Op, T, G, CAP><<<grid, kThreads, smem, s>>>(mp, op, gscale, flags, step);
+      return check_launch("mt_step_tma_kernel");
+    }
+  }
   const int grid = static_cast<int>(tiles < cap ? tiles : cap);
   mt_step_kernel<Op, T, G, CAP, U><<<grid, kThreads, 0, s>>>(mp, op, gscale, flags, step);
   return check_launch("mt_step_kernel");
