@@ -475,8 +475,17 @@ mt_step_kernel(const __grid_constant__ MTParams<CAP> mp, const Op op_in,
 // that are not full or not 16-byte aligned are read from global memory
 // directly.  Same arithmetic, so the same bits.
 // ---------------------------------------------------------------------------
-constexpr int kTmaTile = 2048;
-constexpr int kTmaStages = 4;
+#ifndef OF_TMA_TILE
+#define OF_TMA_TILE 2048
+#endif
+#ifndef OF_TMA_STAGES
+#define OF_TMA_STAGES 4
+#endif
+#ifndef OF_TMA_CTAS
+#define OF_TMA_CTAS 1
+#endif
+constexpr int kTmaTile = OF_TMA_TILE;
+constexpr int kTmaStages = OF_TMA_STAGES;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -511,7 +520,7 @@ struct TmaLayout {
 };
 
 template <class Op, class T, class G, int CAP>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, OF_TMA_CTAS)
 mt_step_tma_kernel(const __grid_constant__ MTParams<CAP> mp, const Op op_in,
                    const float* __restrict__ gscale, uint32_t flags, const StepSrc step) {
   using GV = typename GradVal<G>::type;
@@ -826,7 +835,7 @@ int launch_step_chunk(const of_tensor_list* l, int first, int count, const Op& o
         configured = true;
       }
       const int64_t ttiles = pack<CAP>(l, first, count, mp, kTmaTile);
-      const int64_t tcap = sm_count();
+      const int64_t tcap = static_cast<int64_t>(sm_count()) * OF_TMA_CTAS;
       const int grid = static_cast<int>(ttiles < tcap ? ttiles : tcap);
       mt_step_tma_kernel<Op, T, G, CAP><<<grid, kThreads, smem, s>>>(mp, op, gscale, flags, step);
       return check_launch("mt_step_tma_kernel");
