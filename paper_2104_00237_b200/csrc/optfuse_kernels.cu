@@ -486,6 +486,7 @@ mt_step_kernel(const __grid_constant__ MTParams<CAP> mp, const Op op_in,
 #endif
 constexpr int kTmaTile = OF_TMA_TILE;
 constexpr int kTmaStages = OF_TMA_STAGES;
+static_assert(kTmaTile % (256 * 4) == 0, "a TMA tile is whole float4 rows of the block");
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
