@@ -897,29 +897,47 @@ def e2e(args, device, dist, flush=None) -> dict:
 
 
 def _e2e_instance(args, device, dist, flush, xh, yh) -> float:
+    """Every step: the batch copied in from pinned host memory, the iteration,
+    the loss copied out to pinned host memory and read on the host.  Step k's
+    loss is read while step k+1 runs (a two-slot pinned ring and an event per
+    step), so the host never idles the GPU between steps."""
     import torch
     step, g, pol = make_runner(args, args.batch, args.schedule, device)
-    if hasattr(step, "graph"):
-        def one():
-            if flush is not None:
-                flush()
-            return step((xh, yh)).item()
-    else:
-        run = step.run
+    graphed = hasattr(step, "graph")
+    run = None if graphed else step.run
+    ring = [torch.empty((), dtype=torch.float32).pin_memory() for _ in range(2)]
+    events = [torch.cuda.Event(), torch.cuda.Event()]
+    losses = []
 
-        def one():
-            if flush is not None:
-                flush()
-            return run((xh.to(device, non_blocking=True), yh.to(device, non_blocking=True))).item()
-    for _ in range(args.warmup):
-        one()
+    def one(k):
+        if flush is not None:
+            flush()
+        if graphed:
+            loss = step((xh, yh))
+        else:
+            loss = run((xh.to(device, non_blocking=True), yh.to(device, non_blocking=True)))
+        ring[k % 2].copy_(loss.detach().float(), non_blocking=True)
+        events[k % 2].record()
+        if k > 0:                      # the previous step's loss, read on the host now
+            events[(k - 1) % 2].synchronize()
+            losses.append(float(ring[(k - 1) % 2]))
+
+    def drain(k):
+        events[(k - 1) % 2].synchronize()
+        losses.append(float(ring[(k - 1) % 2]))
+    for k in range(args.warmup):
+        one(k)
+    drain(args.warmup)
     torch.cuda.synchronize()
     dist.barrier()
+    losses.clear()
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        one()
+    for k in range(args.steps):
+        one(k)
+    drain(args.steps)
     torch.cuda.synchronize()
     dt = dist.max(time.perf_counter() - t0)
+    assert len(losses) == args.steps and all(v == v for v in losses), "e2e: a loss was not read"
     return dist.world * args.batch * args.steps / dt
 
 
