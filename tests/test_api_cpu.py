@@ -223,3 +223,20 @@ def test_same_layout_ignores_strides_of_size_one_dims():
     assert not same_layout(a, b)
     assert not same_layout(torch.empty(4), torch.empty(4, dtype=torch.float64))
     assert not same_layout(torch.empty(8)[::2], torch.empty(4))
+
+
+def test_device_step_table_holds_the_hosts_bias_corrections():
+    """OF_FLAG_DEVICE_STEP reads (1 - beta1**t, 1 - beta2**t) from this table:
+    the very Python doubles optim.py:145-146 computes, filled ahead of use."""
+    from paper_2104_00237_b200.optim import DeviceStep
+    pol = of.OptimizerPolicy("adam", beta1=0.9, beta2=0.999)
+    pol.t = 5
+    ds = DeviceStep(pol, torch.device("cpu"))
+    assert ds.filled >= 6 and ds.table.dtype == torch.float64
+    for t in (1, 2, 5, ds.filled - 1):
+        assert float(ds.table[t, 0]) == 1 - 0.9 ** t and float(ds.table[t, 1]) == 1 - 0.999 ** t
+    ds.ensure(ds.filled + 10)
+    t = ds.filled - 1
+    assert float(ds.table[t, 1]) == 1 - 0.999 ** t
+    with pytest.raises(errors.StateError):
+        ds.ensure(DeviceStep.ROWS)
