@@ -424,6 +424,33 @@ class Engine : public std::enable_shared_from_this<Engine> {
 
   // -- profiling -----------------------------------------------------------
   void set_profile(bool on) { profile_ = on; }
+  // A timing event: inside a CUDA-graph capture it becomes an event-record
+  // node (cudaEventRecordExternal), re-recorded by every replay, so the launch
+  // can be timed live inside the replayed iteration.
+  static void record_timing(cudaEvent_t e, cudaStream_t s) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cuda_check(cudaStreamIsCapturing(s, &cs), "cudaStreamIsCapturing");
+    if (cs == cudaStreamCaptureStatusActive)
+      cuda_check(cudaEventRecordWithFlags(e, s, cudaEventRecordExternal), "cudaEventRecordWithFlags");
+    else
+      cuda_check(cudaEventRecord(e, s), "cudaEventRecord");
+  }
+
+  // The last `last` timed launches (ms, elements), events kept (a replayed
+  // graph re-records them).
+  std::vector<std::pair<double, int64_t>> peek_profile(int last) {
+    std::vector<std::pair<double, int64_t>> out;
+    const int n = static_cast<int>(prof_.size());
+    for (int i = n - last < 0 ? 0 : n - last; i < n; ++i) {
+      auto& r = prof_[i];
+      cuda_check(cudaEventSynchronize(r.stop), "cudaEventSynchronize");
+      float ms = 0.f;
+      cuda_check(cudaEventElapsedTime(&ms, r.start, r.stop), "cudaEventElapsedTime");
+      out.emplace_back(ms, r.elems);
+    }
+    return out;
+  }
+
   std::vector<std::pair<double, int64_t>> take_profile() {
     std::vector<std::pair<double, int64_t>> out;
     for (auto& r : prof_) {
@@ -489,7 +516,7 @@ class Engine : public std::enable_shared_from_this<Engine> {
     if (profile_) {
       cuda_check(cudaEventCreate(&a), "cudaEventCreate");
       cuda_check(cudaEventCreate(&b), "cudaEventCreate");
-      cuda_check(cudaEventRecord(a, s), "cudaEventRecord");
+      record_timing(a, s);
     }
     const float* gs = gscale_.defined() ? gscale_.data_ptr<float>() : nullptr;
     const int st = of_policy_step_mt(&G.list, &hp_, gs, flags_, s);
@@ -497,7 +524,7 @@ class Engine : public std::enable_shared_from_this<Engine> {
       throw std::runtime_error(std::string("of_policy_step_mt: ") + of_status_string(st) + " (" +
                                of_last_error() + ")");
     if (profile_) {
-      cuda_check(cudaEventRecord(b, s), "cudaEventRecord");
+      record_timing(b, s);
       prof_.push_back({a, b, G.elems});
     }
     ++launches_;
@@ -641,6 +668,7 @@ PYBIND11_MODULE(_optfuse_engine, m) {
       .def("flush", &Engine::flush)
       .def("set_profile", &Engine::set_profile)
       .def("take_profile", &Engine::take_profile)
+      .def("peek_profile", &Engine::peek_profile)
       .def("launch_group", &Engine::launch_now, py::arg("gi"), py::arg("sync") = true)
       .def_property_readonly("launches", &Engine::launches)
       .def_property_readonly("num_groups", &Engine::num_groups);
