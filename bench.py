@@ -573,7 +573,8 @@ def measure_in_graph(args, device, peaks, flush, reps: int = 20) -> dict:
     tot_bytes = sum(elems) * bytes_per_element(pol.kind, 4)
     gbs = tot_bytes / t / 1e9
     return {"launches_per_step": n, "avg_bytes": tot_bytes / n, "avg_us": t / n * 1e6,
-            "achieved_gbs": gbs, "frac": gbs / peaks["hbm_gbs"]}
+            "achieved_gbs": gbs, "frac": gbs / peaks["hbm_gbs"],
+            "replays": reps, "step_us_min_max": [round(min(ms) * 1e3, 3), round(max(ms) * 1e3, 3)]}
 
 
 def cpu_baseline(args, iters: int) -> dict:
