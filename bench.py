@@ -9,7 +9,7 @@ CIFAR-10-shaped data (3x32x32, 10 classes), SGD-momentum (lr 0.1, momentum
 128 per GPU, channels-last, backward fusion with 1M-element buckets on the
 side stream, the whole iteration replayed from a CUDA graph.  One "step" =
 one training iteration (forward, backward, every parameter updated), with a
-256 MiB L2 flush before it.  The same iteration is also timed with
+256 MiB L2 flush before it (between its event pair and the previous one's).  The same iteration is also timed with
 torch.optim.SGD (foreach, fused), with no update at all (the floor any fusion
 can reach), and under our other schedules, eager and graphed; a batch sweep
 32..512 and the other BASELINE.json configs (C1, C3, C4, C5) are reported
@@ -90,7 +90,7 @@ def parse_args(argv=None):
     ap.add_argument("--extras", default="c1,c3,c4,c5",
                     help="other BASELINE.json configs timed beside the headline ('' to skip)")
     ap.add_argument("--cpu-iters", type=int, default=2, help="CPU baseline sample iterations")
-    ap.add_argument("--instances", type=int, default=3,
+    ap.add_argument("--instances", type=int, default=5,
                     help="independently built model instances timed for the headline and key rows")
     return ap.parse_args(argv)
 
@@ -194,6 +194,8 @@ class Clocks:
 def timed(step, steps: int, warmup: int, dist: Dist, flush=None) -> float:
     """W warm-up steps, then EXACTLY K steps between barrier+synchronize on both
     sides, device-timed with CUDA events on the current stream; max over ranks.
+    With ``flush`` (an L2 flush between timed iterations) each step has its own
+    event pair after the flush, and the flush is not part of the step time.
     Returns ms per step."""
     import torch
     for _ in range(warmup):
@@ -201,21 +203,28 @@ def timed(step, steps: int, warmup: int, dist: Dist, flush=None) -> float:
     torch.cuda.synchronize()
     dist.barrier()
     s = torch.cuda.current_stream()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n = steps if flush is not None else 1
+    e0 = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+    e1 = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
     # a start/end range is process-wide (push/pop ranges are per thread and would
     # miss the backward kernels autograd launches from its own thread):
     # ncu --nvtx --nvtx-include timed selects this region
     rng = torch.cuda.nvtx.range_start("timed")
-    e0.record(s)
-    for _ in range(steps):
+    if flush is None:
+        e0[0].record(s)
+    for i in range(steps):
         if flush is not None:
             flush()
+            e0[i].record(s)
         step()
-    e1.record(s)
+        if flush is not None:
+            e1[i].record(s)
+    if flush is None:
+        e1[0].record(s)
     torch.cuda.synchronize()
     torch.cuda.nvtx.range_end(rng)
     dist.barrier()
-    return dist.max(e0.elapsed_time(e1)) / steps
+    return dist.max(sum(a.elapsed_time(b) for a, b in zip(e0, e1))) / steps
 
 
 def load_peaks() -> dict:
@@ -754,7 +763,7 @@ def run_ours(args) -> dict:
                                    "fused peer-memory kernel per bucket (reduce-scatter + update + "
                                    "all-gather in one kernel over symmetric memory)")
                                   + "; unfused baseline DDP + torch.optim" if args.dp else None),
-                      "l2": "256 MiB buffer zeroed before every timed step (inside the timed region)",
+                      "l2": "256 MiB buffer zeroed before every timed step (outside each step's event pair)",
                       "model_math": ("fp32 parameters/activations; TF32 tensor cores for convolutions "
                                      f"(cudnn.allow_tf32={torch.backends.cudnn.allow_tf32}) and matmuls "
                                      f"(matmul.allow_tf32={torch.backends.cuda.matmul.allow_tf32}); "
@@ -942,8 +951,8 @@ def e2e(args, device, dist, flush=None) -> dict:
     """The headline configuration through the public API, end to end: each
     step copies the batch from pinned host memory to the device and reads the
     loss back (CapturedStep copies into its static buffers, then replays).
-    Wall clock over the K steps, max over ranks; L2 flushed before every step
-    like the device-timed value."""
+    Wall clock over the K steps less the device-timed L2 flushes (one before
+    every step, like the device-timed value), max over ranks."""
     import torch
 
     from paper_2104_00237_b200.models import synthetic_batch
@@ -970,10 +979,15 @@ def _e2e_instance(args, device, dist, flush, xh, yh) -> float:
     ring = [torch.empty((), dtype=torch.float32).pin_memory() for _ in range(2)]
     events = [torch.cuda.Event(), torch.cuda.Event()]
     losses = []
+    # the L2 flush between steps is device-timed and taken out of the wall clock
+    fl = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(max(args.steps, args.warmup))]
 
     def one(k):
         if flush is not None:
+            fl[k][0].record()
             flush()
+            fl[k][1].record()
         if graphed:
             loss = step((xh, yh))
         else:
@@ -998,7 +1012,10 @@ def _e2e_instance(args, device, dist, flush, xh, yh) -> float:
         one(k)
     drain(args.steps)
     torch.cuda.synchronize()
-    dt = dist.max(time.perf_counter() - t0)
+    dt = time.perf_counter() - t0
+    if flush is not None:
+        dt -= sum(a.elapsed_time(b) for a, b in fl[:args.steps]) / 1e3
+    dt = dist.max(dt)
     assert len(losses) == args.steps and all(v == v for v in losses), "e2e: a loss was not read"
     return dist.world * args.batch * args.steps / dt
 

@@ -33,6 +33,19 @@ from .errors import StateError
 _STEP_INDEPENDENT = ("sgd", "sgd-momentum", "adagrad", "rmsprop", "adadelta")
 
 
+_CAPTURE_STREAMS: dict = {}
+
+
+def _capture_stream(device):
+    """One warm-up/capture stream per device, shared by every CapturedStep
+    (captures run one at a time): each new stream that runs a matmul gets its
+    own cuBLAS workspace, kept for the life of the process."""
+    s = _CAPTURE_STREAMS.get(device)
+    if s is None:
+        s = _CAPTURE_STREAMS[device] = torch.cuda.Stream(device)
+    return s
+
+
 class CapturedStep:
     """``step_fn(inputs) -> loss`` captured once, replayed by ``__call__``.
 
@@ -52,7 +65,7 @@ class CapturedStep:
         cur = torch.cuda.current_stream()
         # warm-up and capture stream (a caller whose module stashed autograd
         # nodes on a stream, e.g. DDP, passes that stream)
-        side = stream if stream is not None else torch.cuda.Stream()
+        side = stream if stream is not None else _capture_stream(cur.device)
         side.wait_stream(cur)
         with torch.cuda.stream(side):
             for _ in range(warmup):

@@ -36,11 +36,16 @@ def main():
         loss = F.cross_entropy(net(inp[0]), inp[1])
         loss.backward()
         return loss
-    for _ in range(6):
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 6
+    keep = []
+    for _ in range(n):
         cap = CapturedStep(run, (x, y), warmup=3)
         out["same_instance_recaptured"].append(round(bench.timed(cap, 30, 10, dist, buf.zero_), 4))
-        del cap
-    for _ in range(6):
+        keep.append(cap)       # alive: every capture gets its own pool and stream
+    # the captures again, in order: is the mode a property of the captured graph?
+    out["recaptured_retimed"] = [round(bench.timed(c, 30, 10, dist, buf.zero_), 4) for c in keep]
+    del keep
+    for _ in range(n):
         g2 = of.build_classifier("mobilenet_v2_cifar", device=dev, channels_last=True)
         net = g2.module
         cap = CapturedStep(run, (x, y), warmup=3)

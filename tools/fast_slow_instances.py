@@ -28,7 +28,7 @@ def main():
     x, y = synthetic_batch("mobilenet_v2_cifar", 128, device=dev)
     x = x.contiguous(memory_format=torch.channels_last)
     caps = []
-    for i in range(12):
+    for i in range(30):
         g = of.build_classifier("mobilenet_v2_cifar", device=dev, channels_last=True)
         net = g.module
 
