@@ -375,3 +375,53 @@ def test_copy_mt_many_tensors_any_alignment():
     torch.cuda.synchronize()
     for d, s in zip(dsts, srcs):
         assert torch.equal(d, s)
+
+
+def test_tensor_beyond_2_31_elements():
+    """One 2^31 + 6157-element tensor (26 GB with its gradient and momentum):
+    64-bit element offsets; checked bitwise against the oracle on windows at
+    the head, across the 2^31 boundary and at the ragged tail."""
+    n = (1 << 31) + 6157
+    if torch.cuda.get_device_properties(0).total_memory < 64 << 30:
+        pytest.skip("needs a large-memory GPU")
+    gen = torch.Generator(device=DEV).manual_seed(11)
+    val = torch.randn(n, device=DEV, generator=gen)
+    grad = torch.randn(n, device=DEV, generator=gen)
+    wins = [(0, 4096), ((1 << 31) - 4096, (1 << 31) + 4096), (n - 5000, n)]
+    before = [(val[a:b].cpu().numpy().copy(), grad[a:b].cpu().numpy().copy()) for a, b in wins]
+    p = of.Parameter(0, torch.nn.Parameter(val))
+    del val
+    p.value.grad = grad
+    del grad
+    pol = of.OptimizerPolicy("sgd-momentum", eta=0.1, grad_reset="none")
+    h = optim_ref.Hyper(kind="sgd-momentum", eta=0.1)
+    pol.begin_iteration()
+    pol.step(p)
+    torch.cuda.synchronize()
+    for (a, b), (th, g) in zip(wins, before):
+        optim_ref.step("sgd-momentum", h, th, g, {}, 1)
+        assert p.value[a:b].detach().cpu().numpy().tobytes() == th.tobytes(), (a, b)
+    del p
+    torch.cuda.empty_cache()
+
+
+def test_empty_tensors_in_a_list():
+    """Zero-element parameters beside ordinary ones: skipped by the packer,
+    the others updated bitwise."""
+    rng = np.random.default_rng(8)
+    sizes = [0, 513, 0, 4096, 0, 7]
+    arrs = [rng.standard_normal(s).astype(np.float32) for s in sizes]
+    params = [_param(a, i) for i, a in enumerate(arrs)]
+    pol = of.OptimizerPolicy("adam", eta=1e-3)
+    h = optim_ref.Hyper(kind="adam", eta=1e-3)
+    slots = [dict() for _ in arrs]
+    for s in range(3):
+        pol.begin_iteration()
+        gs = [rng.standard_normal(a.size).astype(np.float32) for a in arrs]
+        for p, g in zip(params, gs):
+            p.value.grad = torch.from_numpy(g).to(DEV)
+        pol.step_params(params)
+        for a, g, sl in zip(arrs, gs, slots):
+            optim_ref.step("adam", h, a, g, sl, s + 1)
+    for p, a in zip(params, arrs):
+        assert p.value.detach().cpu().numpy().tobytes() == a.tobytes()
