@@ -968,8 +968,9 @@ def e2e(args, device, dist, flush=None) -> dict:
 
 
 def _e2e_instance(args, device, dist, flush, xh, yh) -> float:
-    """Every step: the batch copied in from pinned host memory, the iteration,
-    the loss copied out to pinned host memory and read on the host.  Step k's
+    """Every step: the batch copied in from pinned host memory (graphed: staged
+    on a copy stream while the previous replay runs, CapturedStep.stage), the
+    iteration, the loss copied out to pinned host memory and read on the host.  Step k's
     loss is read while step k+1 runs (a two-slot pinned ring and an event per
     step), so the host never idles the GPU between steps."""
     import torch
@@ -989,7 +990,12 @@ def _e2e_instance(args, device, dist, flush, xh, yh) -> float:
             flush()
             fl[k][1].record()
         if graphed:
-            loss = step((xh, yh))
+            # this step's batch was staged (host -> device on the step's copy
+            # stream) while the previous replay ran; stage the next one now
+            if not step._staged:
+                step.stage((xh, yh))
+            loss = step()
+            step.stage((xh, yh))
         else:
             loss = run((xh.to(device, non_blocking=True), yh.to(device, non_blocking=True)))
         ring[k % 2].copy_(loss.detach().float(), non_blocking=True)

@@ -128,6 +128,8 @@ class CapturedStep:
             self.dstep.offset.fill_(-1)     # replay j runs with offset j
         self.replays = 0
         self._t = policy.t if policy is not None else None
+        self._stage = None        # device staging copy of the next call's inputs
+        self._staged = False
 
     def _arg(self):
         return self.static if len(self.static) > 1 else self.static[0]
@@ -146,11 +148,53 @@ class CapturedStep:
             if self.dstep is not None:
                 self.dstep.ensure(pol.t + 1)
         if inputs is not None:
+            if self._staged:
+                raise StateError("inputs were staged for this call; call it without inputs")
             src = inputs if isinstance(inputs, tuple) else (inputs,)
             _copy_into(self.static, src)
+        elif self._staged:
+            cur = torch.cuda.current_stream()
+            cur.wait_event(self._stage_ready)
+            _copy_into(self.static, self._stage)      # on-device, ~1 µs per MB
+            self._stage_free.record(cur)
+            self._staged = False
         self.graph.replay()
         self.replays += 1
         return self.loss
+
+
+    def stage(self, inputs) -> None:
+        """Starts copying the NEXT call's inputs (ideally pinned host tensors)
+        into a device staging buffer on a copy stream, overlapping whatever
+        runs now (typically the previous replay).  The next ``__call__()``
+        without inputs consumes them: one on-device copy into the static
+        inputs, ordered behind the staging copy.  The host tensors must stay
+        unchanged until that call has been issued."""
+        if self._staged:
+            raise StateError("inputs already staged; call the step before staging more")
+        src = inputs if isinstance(inputs, tuple) else (inputs,)
+        if self._stage is None:
+            self._copy_stream = torch.cuda.Stream()
+            self._stage = _empty_like_nested(self.static, self._copy_stream)
+            self._stage_ready = torch.cuda.Event()
+            self._stage_free = torch.cuda.Event()
+            self._stage_free.record()
+        cs = self._copy_stream
+        cs.wait_event(self._stage_free)           # the last staged inputs were consumed
+        with torch.cuda.stream(cs):
+            _copy_into(self._stage, src)
+        self._stage_ready.record(cs)
+        self._staged = True
+
+
+def _empty_like_nested(t, stream):
+    """Allocated on the current stream, also used on ``stream`` (so that its
+    memory is not reused before that stream's copies into it are done)."""
+    if isinstance(t, (tuple, list)):
+        return type(t)(_empty_like_nested(x, stream) for x in t)
+    e = torch.empty_like(t)
+    e.record_stream(stream)
+    return e
 
 
 def _copy_into(dst, src) -> None:
