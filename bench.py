@@ -992,7 +992,7 @@ def _e2e_instance(args, device, dist, flush, xh, yh) -> float:
         if graphed:
             # this step's batch was staged (host -> device on the step's copy
             # stream) while the previous replay ran; stage the next one now
-            if not step._staged:
+            if not step.staged:
                 step.stage((xh, yh))
             loss = step()
             step.stage((xh, yh))

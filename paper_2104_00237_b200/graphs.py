@@ -163,6 +163,11 @@ class CapturedStep:
         return self.loss
 
 
+    @property
+    def staged(self) -> bool:
+        """Inputs are staged for the next call."""
+        return self._staged
+
     def stage(self, inputs) -> None:
         """Starts copying the NEXT call's inputs (ideally pinned host tensors)
         into a device staging buffer on a copy stream, overlapping whatever
