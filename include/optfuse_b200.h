@@ -183,6 +183,28 @@ typedef struct of_peer_bucket {
 int of_dp_step_peer(const of_peer_bucket* bucket, const of_hparams* hp,
                     const float* grad_scale_dev, uint32_t flags, void* stream);
 
+/* The same bucket step over NVLink SHARP (NVLS) multicast: the shard's gradient is
+ * read once through the multicast address with an in-switch sum
+ * (multimem.ld_reduce), the new parameters and the zeroed gradient are written
+ * once to every peer through multicast stores (multimem.st).  fp32 only.  The
+ * switch's summation order is its own: bitwise equal to of_dp_step_peer at
+ * world 1, tolerance-equal beyond.  Same barriers, flags and errors as
+ * of_dp_step_peer (replaces the same reduce-scatter/all-gather pair). */
+typedef struct of_mc_bucket {
+  int32_t world;           /* W, 1 .. OF_MAX_PEERS */
+  int32_t rank;
+  void* mc_grad;           /* multicast address of the flat gradient buffer */
+  void* mc_param;          /* multicast address of the flat parameter buffer */
+  void* local_param;       /* this rank's flat parameter buffer (unicast) */
+  void* state0;            /* history of the shard */
+  void* state1;
+  int64_t shard_begin;     /* multiple of 4 */
+  int64_t shard_len;       /* multiple of 4 */
+} of_mc_bucket;
+
+int of_dp_step_multicast(const of_mc_bucket* bucket, const of_hparams* hp,
+                         const float* grad_scale_dev, uint32_t flags, void* stream);
+
 /* dst[i] <- src[i] (nbytes[i] bytes each) for n tensors in one launch per 256
  * (multi-tensor copy; CUDA-graph forward fusion routes each replay's gradients
  * to the buffers the next replay's updates read with it). */

@@ -31,7 +31,7 @@ KIND_CODES = {"sgd": 0, "sgd-momentum": 1, "adagrad": 2, "rmsprop": 3, "adadelta
 SYMBOLS = ("of_abi_version", "of_status_string", "of_last_error", "of_launch_count",
            "of_policy_step_mt", "of_sgdm_mt", "of_adam_mt", "of_step_advance", "of_dp_step_peer",
            "of_sqnorm_workspace_len", "of_sqnorm_mt", "of_clip_coef", "of_exact_matmul",
-           "of_copy_mt")
+           "of_copy_mt", "of_dp_step_multicast")
 
 _vp = ctypes.c_void_p
 _PP = ctypes.POINTER(ctypes.c_void_p)
@@ -61,6 +61,13 @@ class OfPeerBucket(ctypes.Structure):
     _fields_ = [("world", ctypes.c_int32), ("rank", ctypes.c_int32),
                 ("param_dtype", ctypes.c_int32), ("grad_dtype", ctypes.c_int32),
                 ("peer_grad", _PP), ("peer_param", _PP), ("master", _vp),
+                ("state0", _vp), ("state1", _vp),
+                ("shard_begin", ctypes.c_int64), ("shard_len", ctypes.c_int64)]
+
+
+class OfMcBucket(ctypes.Structure):
+    _fields_ = [("world", ctypes.c_int32), ("rank", ctypes.c_int32),
+                ("mc_grad", _vp), ("mc_param", _vp), ("local_param", _vp),
                 ("state0", _vp), ("state1", _vp),
                 ("shard_begin", ctypes.c_int64), ("shard_len", ctypes.c_int64)]
 
@@ -101,6 +108,9 @@ def lib():
     so.of_dp_step_peer.restype = ctypes.c_int
     so.of_dp_step_peer.argtypes = [ctypes.POINTER(OfPeerBucket), ctypes.POINTER(OfHparams), _vp,
                                    ctypes.c_uint32, _vp]
+    so.of_dp_step_multicast.restype = ctypes.c_int
+    so.of_dp_step_multicast.argtypes = [ctypes.POINTER(OfMcBucket), ctypes.POINTER(OfHparams), _vp,
+                                        ctypes.c_uint32, _vp]
     so.of_copy_mt.restype = ctypes.c_int
     so.of_copy_mt.argtypes = [_PP, _PP, ctypes.POINTER(ctypes.c_int64), ctypes.c_int, _vp]
     so.of_exact_matmul.restype = ctypes.c_int

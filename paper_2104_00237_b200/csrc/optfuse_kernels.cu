@@ -1018,6 +1018,68 @@ int dispatch_peer(const PeerParams& pp, const of_hparams* hp, const float* gscal
   });
 }
 
+// ---------------------------------------------------------------------------
+// The peer step over NVLS multicast (of_dp_step_multicast): one in-switch
+// reduced load of the shard's gradient, one multicast store of the new
+// parameters and of the zeroed gradient, whatever the world size.
+// ---------------------------------------------------------------------------
+struct McParams {
+  float* mc_grad;
+  float* mc_param;
+  const float* local_param;
+  float* s0;
+  float* s1;
+  int64_t begin, len;
+};
+
+__device__ __forceinline__ float4 mc_ld_reduce_add4(const float* p) {
+  float4 r;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p) : "memory");
+  return r;
+}
+
+__device__ __forceinline__ void mc_st4(float* p, float a, float b, float c, float d) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};"
+               :: "l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+
+template <class Op>
+__global__ void __launch_bounds__(kThreads)
+mc_step_kernel(const __grid_constant__ McParams mp, const Op op_in,
+               const float* __restrict__ gscale, const StepSrc step) {
+  Op op = op_in;
+  if (step.offset != nullptr) {
+    int64_t t = step.t_base + *step.offset;
+    t = t < 1 ? 1 : (t >= step.rows ? step.rows - 1 : t);
+    op.set_step(step.table[2 * t], step.table[2 * t + 1]);
+  }
+  const bool has_scale = gscale != nullptr;
+  const float scale = has_scale ? *gscale : 1.f;
+  const int64_t nvec = mp.len / kVec;
+  for (int64_t v = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; v < nvec;
+       v += static_cast<int64_t>(gridDim.x) * kThreads) {
+    const int64_t e = mp.begin + kVec * v;
+    const int64_t o = kVec * v;
+    const float4 g4 = mc_ld_reduce_add4(mp.mc_grad + e);
+    const float g[4] = {g4.x, g4.y, g4.z, g4.w};
+    float p[4], a[4], b[4];
+    ld4(mp.local_param + e, p);
+    if (Op::kSlots >= 1) ld4(mp.s0 + o, a);
+    if (Op::kSlots >= 2) ld4(mp.s1 + o, b);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float gk = g[k];
+      if (has_scale) gk = o_mul(gk, scale);
+      op(p[k], gk, a[k], b[k]);
+    }
+    if (Op::kSlots >= 1) st4(mp.s0 + o, a);
+    if (Op::kSlots >= 2) st4(mp.s1 + o, b);
+    mc_st4(mp.mc_param + e, p[0], p[1], p[2], p[3]);
+    mc_st4(mp.mc_grad + e, 0.f, 0.f, 0.f, 0.f);
+  }
+}
+
 template <class G, int CAP>
 int launch_sqnorm_chunk(const of_tensor_list* l, int first, int count, double* ws, int64_t ws_len,
                         double* out, int accumulate, cudaStream_t s) {
@@ -1276,6 +1338,58 @@ int of_dp_step_peer(const of_peer_bucket* b, const of_hparams* hp, const float* 
   if (b->param_dtype == OF_F32) return dispatch_peer<float, float, false>(pp, hp, grad_scale_dev, flags, s);
   if (b->param_dtype == OF_F64) return dispatch_peer<double, double, false>(pp, hp, grad_scale_dev, flags, s);
   return fail(OF_ERR_UNSUPPORTED, "param dtype %d", b->param_dtype);
+}
+
+int of_dp_step_multicast(const of_mc_bucket* b, const of_hparams* hp, const float* grad_scale_dev,
+                         uint32_t flags, void* stream) {
+  g_err[0] = '\0';
+  if (!b || !hp) return fail(OF_ERR_INVALID, "bucket or hparams is NULL");
+  const int slots = slots_of(hp->kind);
+  if (slots < 0) return fail(OF_ERR_INVALID, "unknown optimizer kind %d", hp->kind);
+  if (flags & ~(OF_FLAG_DEVICE_STEP))
+    return fail(OF_ERR_INVALID, "flags 0x%x not supported by the multicast step", flags);
+  if (!(hp->eta > 0.0)) return fail(OF_ERR_INVALID, "step size must be > 0, got %g", hp->eta);
+  if (flags & OF_FLAG_DEVICE_STEP) {
+    if (!hp->step_offset_dev || !hp->step_table_dev || hp->step_table_rows < 2)
+      return fail(OF_ERR_INVALID, "OF_FLAG_DEVICE_STEP needs step_offset_dev and a step table");
+  } else if ((hp->kind == OF_ADAM || hp->kind == OF_ADAMW) &&
+             (hp->bias_correction1 == 0.0 || hp->bias_correction2 == 0.0)) {
+    return fail(OF_ERR_INVALID, "adam bias corrections must be non-zero (step index t >= 1)");
+  }
+  if (b->world < 1 || b->world > OF_MAX_PEERS)
+    return fail(OF_ERR_INVALID, "world %d outside [1, %d]", b->world, OF_MAX_PEERS);
+  if (b->rank < 0 || b->rank >= b->world)
+    return fail(OF_ERR_INVALID, "rank %d outside [0, %d)", b->rank, b->world);
+  if (b->shard_begin < 0 || b->shard_len < 0 || (b->shard_begin % 4) || (b->shard_len % 4))
+    return fail(OF_ERR_INVALID, "shard [%lld, +%lld) must be non-negative multiples of 4",
+                (long long)b->shard_begin, (long long)b->shard_len);
+  if (!b->mc_grad || !b->mc_param || !b->local_param)
+    return fail(OF_ERR_INVALID, "multicast or local buffer is NULL");
+  if ((reinterpret_cast<uintptr_t>(b->mc_grad) | reinterpret_cast<uintptr_t>(b->mc_param) |
+       reinterpret_cast<uintptr_t>(b->local_param)) & 15)
+    return fail(OF_ERR_INVALID, "multicast buffers must be 16-byte aligned");
+  if (slots >= 1 && !b->state0) return fail(OF_ERR_INVALID, "kind needs state0");
+  if (slots >= 2 && !b->state1) return fail(OF_ERR_INVALID, "kind needs state1");
+  McParams mp;
+  mp.mc_grad = static_cast<float*>(b->mc_grad);
+  mp.mc_param = static_cast<float*>(b->mc_param);
+  mp.local_param = static_cast<const float*>(b->local_param);
+  mp.s0 = static_cast<float*>(b->state0);
+  mp.s1 = static_cast<float*>(b->state1);
+  mp.begin = b->shard_begin;
+  mp.len = b->shard_len;
+  const StepSrc step = step_source(hp, flags);
+  const int64_t nvec = mp.len / kVec;
+  if (nvec == 0) return OF_OK;
+  int64_t grid = (nvec + kThreads - 1) / kThreads;
+  int64_t cap = static_cast<int64_t>(sm_count()) * kCtasPerSm;
+  if (hp->max_ctas > 0 && hp->max_ctas < cap) cap = hp->max_ctas;
+  if (grid > cap) grid = cap;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  return with_op<float>(hp, [&](auto op) {
+    mc_step_kernel<decltype(op)><<<static_cast<int>(grid), kThreads, 0, s>>>(mp, op, grad_scale_dev, step);
+    return check_launch("mc_step_kernel");
+  });
 }
 
 }  // extern "C"

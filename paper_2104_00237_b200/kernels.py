@@ -123,6 +123,30 @@ def dp_step_peer(pb: PeerBucket, hp: nat.OfHparams, grad_scale, flags: int, stre
         nat.check(st, "of_dp_step_peer")
 
 
+class McBucket:
+    """Host ``of_mc_bucket`` of one data-parallel bucket over NVLS multicast
+    (multicast addresses of the flat gradient/parameter buffers, fixed)."""
+
+    __slots__ = ("struct", "ref")
+
+    def __init__(self, world: int, rank: int, mc_grad_ptr: int, mc_param_ptr: int, local_param,
+                 state0, state1, shard_begin: int, shard_len: int):
+        def ptr(t):
+            return t.data_ptr() if t is not None else None
+        self.struct = nat.OfMcBucket(world, rank, mc_grad_ptr, mc_param_ptr, ptr(local_param),
+                                     ptr(state0), ptr(state1), shard_begin, shard_len)
+        self.ref = ctypes.byref(self.struct)
+
+
+def dp_step_multicast(mb: McBucket, hp: nat.OfHparams, grad_scale, flags: int, stream) -> None:
+    """of_dp_step_multicast: the bucket step with an in-switch reduced gradient
+    load and multicast parameter/gradient stores (fp32)."""
+    gs = grad_scale.data_ptr() if grad_scale is not None else None
+    st = nat.lib().of_dp_step_multicast(mb.ref, ctypes.byref(hp), gs, flags, _handle(stream))
+    if st:
+        nat.check(st, "of_dp_step_multicast")
+
+
 class CopyList:
     """Fixed (dst, src) tensor pairs for ``of_copy_mt`` (pointers captured once)."""
 

@@ -425,3 +425,137 @@ def test_empty_tensors_in_a_list():
             optim_ref.step("adam", h, a, g, sl, s + 1)
     for p, a in zip(params, arrs):
         assert p.value.detach().cpu().numpy().tobytes() == a.tobytes()
+
+
+class _Multicast1:
+    """A one-device NVLS multicast object bound to a fresh physical allocation
+    (CUDA driver API): ``uva`` is the unicast mapping, ``mva`` the multicast
+    one.  None of torch's symmetric memory: it builds no multicast object for
+    a single rank."""
+
+    def __init__(self, nbytes: int):
+        from cuda.bindings import driver as d
+        self.d = d
+
+        def ok(r):
+            err, *rest = r if isinstance(r, tuple) else (r,)
+            if err != d.CUresult.CUDA_SUCCESS:
+                raise RuntimeError(str(err))
+            return rest[0] if len(rest) == 1 else rest
+        self.ok = ok
+        torch.zeros(1, device=DEV)                     # primary context current
+        dev = ok(d.cuDeviceGet(torch.cuda.current_device()))
+        if not ok(d.cuDeviceGetAttribute(
+                d.CUdevice_attribute.CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, dev)):
+            pytest.skip("no multicast support")
+        fd = d.CUmemAllocationHandleType.CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR
+        mp = d.CUmulticastObjectProp()
+        mp.numDevices = 1
+        mp.handleTypes = fd
+        mp.size = nbytes
+        gran = ok(d.cuMulticastGetGranularity(
+            mp, d.CUmulticastGranularity_flags.CU_MULTICAST_GRANULARITY_RECOMMENDED))
+        size = (nbytes + gran - 1) // gran * gran
+        mp.size = size
+        self.size = size
+        err, mc = d.cuMulticastCreate(mp)
+        if err != d.CUresult.CUDA_SUCCESS:
+            # the single-GPU boxes report multicast support but refuse to
+            # create a one-device multicast object (CUDA_ERROR_INVALID_VALUE)
+            pytest.skip(f"cuMulticastCreate: {err}")
+        self.mc = mc
+        ok(d.cuMulticastAddDevice(self.mc, dev))
+        ap = d.CUmemAllocationProp()
+        ap.type = d.CUmemAllocationType.CU_MEM_ALLOCATION_TYPE_PINNED
+        ap.requestedHandleTypes = fd
+        ap.location.type = d.CUmemLocationType.CU_MEM_LOCATION_TYPE_DEVICE
+        ap.location.id = int(torch.cuda.current_device())
+        self.mem = ok(d.cuMemCreate(size, ap, 0))
+        ok(d.cuMulticastBindMem(self.mc, 0, self.mem, 0, size, 0))
+        acc = d.CUmemAccessDesc()
+        acc.location = ap.location
+        acc.flags = d.CUmemAccess_flags.CU_MEM_ACCESS_FLAGS_PROT_READWRITE
+        self.uva = ok(d.cuMemAddressReserve(size, gran, 0, 0))
+        ok(d.cuMemMap(self.uva, size, 0, self.mem, 0))
+        ok(d.cuMemSetAccess(self.uva, size, [acc], 1))
+        self.mva = ok(d.cuMemAddressReserve(size, gran, 0, 0))
+        ok(d.cuMemMap(self.mva, size, 0, self.mc, 0))
+        ok(d.cuMemSetAccess(self.mva, size, [acc], 1))
+
+    def write(self, arr: np.ndarray) -> None:
+        torch.cuda.synchronize()
+        self.ok(self.d.cuMemcpyHtoD(self.uva, arr.ctypes.data, arr.nbytes))
+
+    def read(self, n: int) -> np.ndarray:
+        torch.cuda.synchronize()
+        out = np.empty(n, dtype=np.float32)
+        self.ok(self.d.cuMemcpyDtoH(out.ctypes.data, self.uva, out.nbytes))
+        return out
+
+    def close(self) -> None:
+        d = self.d
+        for va in (self.mva, self.uva):
+            d.cuMemUnmap(va, self.size)
+            d.cuMemAddressFree(va, self.size)
+        d.cuMulticastUnbind(self.mc, torch.cuda.current_device(), 0, self.size)
+        d.cuMemRelease(self.mem)
+        d.cuMemRelease(self.mc)
+
+
+@pytest.mark.parametrize("kind", ["sgd-momentum", "adam"])
+def test_multicast_step_world1_against_oracle(kind):
+    """of_dp_step_multicast through a real NVLS multicast object of one GPU:
+    the in-switch reduced gradient load, the update and the multicast
+    parameter and zero-gradient stores, bit for bit against the oracle (two
+    steps, the shard in the middle of the buffer)."""
+    n, begin, S = 4 * 1000, 4 * 100, 4 * 700
+    gm, pm = _Multicast1(4 * n), _Multicast1(4 * n)
+    try:
+        rng = np.random.default_rng(12)
+        theta0 = rng.standard_normal(n).astype(np.float32)
+        grads = [rng.standard_normal(n).astype(np.float32) for _ in range(2)]
+        pm.write(theta0)
+        names = optim_ref.SLOTS[kind]
+        states = [torch.zeros(S, device=DEV) for _ in names] + [None, None]
+        eta, wd = ETA[kind], 1e-3
+        mb = kernels.McBucket(1, 0, int(gm.mva), int(pm.mva), None, states[0], states[1], begin, S)
+        mb.struct.local_param = int(pm.uva)
+        for t in (1, 2):
+            gm.write(grads[t - 1])
+            kernels.dp_step_multicast(mb, kernels.hparams(kind, eta, 0.9, wd, 1e-8, 0.9, 0.999,
+                                                          0.9, t), None, 0, None)
+            g = gm.read(n)
+            assert not g[begin:begin + S].any(), "shard gradient not zeroed"
+            assert g[:begin].tobytes() == grads[t - 1][:begin].tobytes()
+        theta = theta0[begin:begin + S].copy()
+        slots = {}
+        h = optim_ref.Hyper(kind=kind, eta=eta, weight_decay=wd)
+        for t in (1, 2):
+            optim_ref.step(kind, h, theta, grads[t - 1][begin:begin + S].copy(), slots, t)
+        got = pm.read(n)
+        assert got[begin:begin + S].tobytes() == theta.tobytes()
+        assert got[:begin].tobytes() == theta0[:begin].tobytes()
+        for k, name in enumerate(names):
+            assert states[k].cpu().numpy().tobytes() == slots[name].tobytes(), name
+    finally:
+        gm.close()
+        pm.close()
+
+
+def test_multicast_step_argument_errors():
+    """of_dp_step_multicast rejects bad buckets before any launch."""
+    st = torch.zeros(8, device=DEV)
+    buf = torch.zeros(64, device=DEV)
+    hp = kernels.hparams("sgd-momentum", 0.1, 0.9, 0.0, 1e-8, 0.9, 0.999, 0.9, 1)
+    cases = [
+        kernels.McBucket(1, 0, buf.data_ptr(), buf.data_ptr(), buf, st, None, 2, 8),      # begin % 4
+        kernels.McBucket(1, 1, buf.data_ptr(), buf.data_ptr(), buf, st, None, 0, 8),      # rank
+        kernels.McBucket(1, 0, 0, buf.data_ptr(), buf, st, None, 0, 8),                   # NULL mc
+        kernels.McBucket(1, 0, buf.data_ptr() + 4, buf.data_ptr(), buf, st, None, 0, 8),  # align
+        kernels.McBucket(1, 0, buf.data_ptr(), buf.data_ptr(), buf, None, None, 0, 8),    # state0
+    ]
+    n0 = nat.launch_count()
+    for mb in cases:
+        with pytest.raises(Exception):
+            kernels.dp_step_multicast(mb, hp, None, 0, None)
+    assert nat.launch_count() == n0
