@@ -15,7 +15,7 @@ dev = torch.device("cuda:0")
 peaks = bench.load_peaks()
 buf = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
 out = {}
-for bucket in (1 << 20, 1 << 18):
+for bucket in (1 << 22, 1 << 20, 1 << 18):
     args.bucket_elems = bucket
     out[str(bucket)] = bench.measure_in_graph(args, dev, peaks, buf.zero_, reps=40)
 print(json.dumps(out))
