@@ -5,28 +5,30 @@
 
 Workload (N=1): configs[1] of BASELINE.json -- MobileNetV2 on synthetic
 CIFAR-10-shaped data (3x32x32, 10 classes), SGD-momentum (lr 0.1, momentum
-0.9, weight decay 5e-4), fp32 weights (TF32 convolutions and matmuls), batch
-128 per GPU, channels-last, backward fusion with 1M-element buckets on the
-side stream, the whole iteration replayed from a CUDA graph.  One "step" =
-one training iteration (forward, backward, every parameter updated), with a
-256 MiB L2 flush before it (between its event pair and the previous one's).  The same iteration is also timed with
-torch.optim.SGD (foreach, fused), with no update at all (the floor any fusion
-can reach), and under our other schedules, eager and graphed; a batch sweep
-32..512 and the other BASELINE.json configs (C1, C3, C4, C5) are reported
-beside the headline.  N>1 (torchrun): the data-parallel path (dp.py, NCCL
-reduce-scatter -> sharded update -> all-gather per bucket, captured in the
-graph) against DDP + torch.optim; --force-dp runs that path at N=1.
+0.9, weight decay 5e-4), true fp32 (TF32 off for convolutions and matmuls),
+batch 128 per GPU, channels-last, backward fusion with 1M-element buckets on
+the side stream, the whole iteration replayed from a CUDA graph.  One "step"
+= one training iteration (forward, backward, every parameter updated), with a
+256 MiB L2 flush before it (outside its event pair).  Its same-mode
+comparators -- our own unfused update (ours:baseline), forward fusion,
+torch.optim.SGD (foreach, fused) and forward+backward with no update (the
+floor any fusion can reach) -- are built --instances times each, interleaved
+instance by instance, and every row is the median over its instances.
+N>1 (torchrun): the data-parallel path (dp.py, NCCL reduce-scatter ->
+sharded update -> all-gather per bucket, captured in the graph) against
+DDP + torch.optim; --force-dp runs that path at N=1.
 
-Prints ONE JSON line (rank 0).  ``value`` = images/s over all ranks with
-inputs resident in HBM, device-timed with CUDA events (max over ranks),
-median of 3 independently built instances; ``e2e`` = the same through the
-public API with pinned-host inputs copied in and the loss read back every
-step; ``roofline`` = the update kernel's average launch duration on its
-stream (back-to-back replay of one iteration's launches) as algorithmic HBM
-bandwidth against MEASURED_PEAKS.json, with the ncu DRAM traffic per launch
-(profiles/ncu_traffic.json) and standalone single-pass figures for the
-C2-C5 parameter sets; ``cpu_baseline`` / ``cpu_update_baseline`` = the
-reference's CPU path (oracle port) on the host cores.
+Prints ONE compact JSON line (rank 0, < 2 KB).  ``value`` = images/s over all
+ranks with inputs resident in HBM, device-timed with CUDA events (max over
+ranks); ``unfused`` = the comparators' medians and the speed-ups against
+them; ``e2e`` = the same step through the public API with pinned-host inputs
+copied in and the loss read back every step; ``roofline`` = the update
+kernel's average launch duration, timed live inside the replayed headline
+graph, as algorithmic HBM bandwidth against MEASURED_PEAKS.json, with the ncu
+DRAM traffic per launch (profiles/ncu_traffic.json); ``cpu_baseline`` = the
+reference's CPU path (oracle port) on the host cores.  Every row, instance
+and diagnostic (batch sweep --sweep, the other configs --extras c1,c3,c4,c5,
+standalone single-launch rooflines) goes to --extras-out.
 
 ``--impl reference`` times the reference's CPU implementation of the path
 (oracle port of optim.py + torch-CPU forward/backward) on the same workload.
@@ -49,9 +51,6 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "train iter time & images/sec (fused vs unfused) at 1/2/4/8 B200; update HBM GB/s"
 UNIT = "images/s"
-WORKLOAD = ("C2: MobileNetV2 (torchvision, 10 classes) on synthetic CIFAR-10 shape 3x32x32, "
-            "SGD-momentum lr 0.1 m 0.9 wd 5e-4, fp32")
-
 
 def parse_args(argv=None):
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
@@ -73,11 +72,12 @@ def parse_args(argv=None):
                          "MobileNetV2's 2.24 M parameters in 3 launches of >= 4 MB, the smallest "
                          "size that leaves the kernel's ~4 us latency floor, still overlapped "
                          "with the backward of the earlier layers)")
-    ap.add_argument("--sweep", default="32,64,256,512", help="extra per-GPU batches ('' to skip)")
     ap.add_argument("--graphs", type=int, default=1,
                     help="1: capture each iteration (ours and the torch baseline) as a CUDA graph")
     ap.add_argument("--channels-last", type=int, default=1, help="1: NHWC model and inputs")
-    ap.add_argument("--no-extras", action="store_true", help="headline only (for profilers)")
+    ap.add_argument("--tf32", type=int, default=0,
+                    help="1: TF32 tensor cores for convolutions and matmuls (every arm; the line "
+                         "then says dtype tf32).  Default 0: true fp32")
     ap.add_argument("--dp-graphs", type=int, default=1,
                     help="1: capture data-parallel iterations (NCCL collectives included) as CUDA "
                          "graphs too (0: eager data parallel)")
@@ -87,11 +87,20 @@ def parse_args(argv=None):
     ap.add_argument("--force-dp", action="store_true",
                     help="run the data-parallel code path (NCCL process group, DataParallelFusion, "
                          "DDP baselines) even at one GPU: the N>1 path's smoke test")
-    ap.add_argument("--extras", default="c1,c3,c4,c5",
-                    help="other BASELINE.json configs timed beside the headline ('' to skip)")
-    ap.add_argument("--cpu-iters", type=int, default=2, help="CPU baseline sample iterations")
     ap.add_argument("--instances", type=int, default=5,
-                    help="independently built model instances timed for the headline and key rows")
+                    help="independently built instances of every arm, interleaved; rows are medians")
+    ap.add_argument("--sweep", default="", help="extra per-GPU batches, e.g. 32,64,256,512")
+    ap.add_argument("--extras", default="",
+                    help="other BASELINE.json configs to time, e.g. c1,c3,c4,c5 (written to --extras-out)")
+    ap.add_argument("--standalone", type=int, default=1,
+                    help="1: standalone single-launch roofline of the C2-C5 parameter sets (extras)")
+    ap.add_argument("--extras-out", default="gpurun_out/bench_extras.json",
+                    help="where every row, instance and diagnostic goes ('' = nowhere); the "
+                         "printed line stays compact")
+    ap.add_argument("--headline-only", action="store_true",
+                    help="time the headline arm only, nothing else (for profilers)")
+    ap.add_argument("--cpu-iters", type=int, default=10, help="CPU baseline: timed iterations")
+    ap.add_argument("--cpu-warmup", type=int, default=2, help="CPU baseline: warm-up iterations")
     return ap.parse_args(argv)
 
 
@@ -586,16 +595,19 @@ def measure_in_graph(args, device, peaks, flush, reps: int = 20) -> dict:
             "replays": reps, "step_us_min_max": [round(min(ms) * 1e3, 3), round(max(ms) * 1e3, 3)]}
 
 
-def cpu_baseline(args, iters: int) -> dict:
+def cpu_baseline(args) -> dict:
+    """The reference arm's measurement (same function, same workload) on a
+    bounded sample: W warm-up + K timed iterations on all host cores."""
     from oracle import timing
-    r = timing.cpu_training_sample(args.model, args.batch, iters, "sgd-momentum",
-                                   dict(eta=0.1, alpha=0.9, weight_decay=5e-4))
+    r = timing.cpu_training_sample(args.model, args.batch, args.cpu_iters, "sgd-momentum",
+                                   dict(eta=0.1, alpha=0.9, weight_decay=5e-4),
+                                   warmup=args.cpu_warmup)
     return {"value": round(r["images_per_s"], 3), "unit": UNIT, "cores": r["threads"],
             "kind": "port",
-            "sample": (f"{iters} iterations at batch {args.batch}: torch-CPU forward/backward on "
-                       f"{r['threads']} threads ({r['fwd_bwd_ms']:.0f} ms) + reference update "
-                       f"(oracle port of optim.py, numpy, 1 thread, {r['update_ms']:.1f} ms "
-                       f"over {r['update_elems']} params)")}
+            "sample": (f"{args.cpu_warmup}+{args.cpu_iters} iterations at batch {args.batch}, "
+                       f"pinned to {r['threads']} cores: torch-CPU fwd/bwd "
+                       f"{r['fwd_bwd_ms']:.0f} ms + reference update (numpy oracle port of "
+                       f"optim.py, 1 thread) {r['update_ms']:.1f} ms")}
 
 
 def cpu_update_baseline(std: dict) -> dict:
@@ -617,60 +629,6 @@ def cpu_update_baseline(std: dict) -> dict:
     return out
 
 
-def _variants_c2(world: int, dp_graphs: bool = False):
-    """(name, schedule, workers, grad_reset, torch optimizer, bucket, CUDA graph, channels-last)"""
-    K = 1 << 18
-    LB = "fwd+bwd only (no update: lower bound)"
-    v = [("torch.optim.SGD(foreach)", "baseline", None, None, "foreach", None, False, False),
-         (LB, "baseline", None, None, "none", None, False, False),
-         ("graph:" + LB, "baseline", None, None, "none", None, True, False),
-         ("cl:graph:" + LB, "baseline", None, None, "none", None, True, True),
-         ("torch.optim.SGD(fused)", "baseline", None, None, "fused", None, False, False),
-         ("ours:baseline", "baseline", None, None, None, None, False, False),
-         ("ours:forward-fusion(per-layer)", "forward-fusion", None, None, None, 0, False, False),
-         ("ours:forward-fusion(bucket=256K)", "forward-fusion", None, None, None, K, False, False),
-         ("ours:backward-fusion(w=1,per-layer)", "backward-fusion", 1, None, None, 0, False, False),
-         ("ours:backward-fusion(w=2,per-layer)", "backward-fusion", 2, None, None, 0, False, False),
-         ("ours:backward-fusion(w=1,bucket=256K)", "backward-fusion", 1, None, None, K, False, False),
-         ("ours:backward-fusion(w=2,bucket=256K)", "backward-fusion", 2, None, None, K, False, False),
-         ("ours:backward-fusion(w=2,bucket=256K,zero)", "backward-fusion", 2, "zero", None, K, False, False),
-         ("graph:torch.optim.SGD(foreach)", "baseline", None, None, "foreach", None, True, False),
-         ("graph:torch.optim.SGD(fused)", "baseline", None, None, "fused", None, True, False),
-         ("graph:ours:baseline", "baseline", None, None, None, None, True, False),
-         ("graph:ours:forward-fusion(bucket=256K)", "forward-fusion", None, None, None, K, True, False),
-         ("graph:ours:backward-fusion(w=2,per-layer)", "backward-fusion", 2, None, None, 0, True, False),
-         ("graph:ours:backward-fusion(w=2,bucket=256K)", "backward-fusion", 2, None, None, K, True, False),
-         ("cl:torch.optim.SGD(foreach)", "baseline", None, None, "foreach", None, False, True),
-         ("cl:ours:backward-fusion(w=2,bucket=256K)", "backward-fusion", 2, None, None, K, False, True),
-         ("cl:graph:torch.optim.SGD(foreach)", "baseline", None, None, "foreach", None, True, True),
-         ("cl:graph:ours:backward-fusion(w=2,bucket=256K)", "backward-fusion", 2, None, None, K, True, True),
-         ("cl:graph:ours:forward-fusion(bucket=256K)", "forward-fusion", None, None, None, K, True, True),
-         ("cl:graph:ours:backward-fusion(w=2,bucket=1M)", "backward-fusion", 2, None, None, 4 * K, True, True),
-         ("cl:graph:ours:backward-fusion(w=2,bucket=4M)", "backward-fusion", 2, None, None, 16 * K, True, True),
-         ("cl:graph:ours:backward-fusion(w=1,bucket=256K)", "backward-fusion", 1, None, None, K, True, True),
-         ("cl:graph:ours:forward-fusion(bucket=1M)", "forward-fusion", None, None, None, 4 * K, True, True),
-         ("cl:graph:ours:forward-fusion(bucket=256K,prefetch)", "forward-fusion", 2, None, None, K, True, True),
-         ("cl:graph:ours:forward-fusion(bucket=256K,prefetch=all)", "forward-fusion", -3, None, None, K, True, True),
-         ("ours:forward-fusion(bucket=256K,prefetch)", "forward-fusion", 2, None, None, K, False, False)]
-    if world > 1 and not dp_graphs:
-        v = [x for x in v if not x[6]]
-    return v
-
-
-KEY_ROWS = ("torch.optim.SGD(foreach)", "ours:backward-fusion(w=2,bucket=256K)",
-            "ours:forward-fusion(bucket=256K)", "graph:torch.optim.SGD(foreach)",
-            "graph:ours:backward-fusion(w=2,bucket=256K)", "cl:graph:torch.optim.SGD(foreach)",
-            "cl:graph:ours:backward-fusion(w=2,bucket=256K)", "cl:graph:ours:forward-fusion(bucket=256K)",
-            "cl:graph:ours:backward-fusion(w=2,bucket=1M)",
-            # the floors vary with cuDNN's per-instance algorithm choice as much as the rows
-            "fwd+bwd only (no update: lower bound)", "graph:fwd+bwd only (no update: lower bound)",
-            "cl:graph:fwd+bwd only (no update: lower bound)")
-SWEEP_ROWS = ("torch.optim.SGD(foreach)", "ours:forward-fusion(bucket=256K)",
-              "graph:fwd+bwd only (no update: lower bound)",
-              "ours:backward-fusion(w=2,bucket=256K)", "graph:torch.optim.SGD(foreach)",
-              "graph:ours:backward-fusion(w=2,bucket=256K)", "graph:ours:forward-fusion(bucket=256K)")
-
-
 def _speedups(row: dict) -> None:
     """Speed-ups against the matching unfused torch baseline (same graph /
     layout mode), and the share of the unfused update phase each schedule
@@ -690,11 +648,51 @@ def _speedups(row: dict) -> None:
             v["speedup_vs_unfused_same_mode"] = round(base["ms_per_step"] / v["ms_per_step"], 4)
         if eager:
             v["speedup_vs_eager_torch_foreach"] = round(eager["ms_per_step"] / v["ms_per_step"], 4)
+        ours = row.get(mode + "ours:baseline")
+        if ours and k.startswith(mode + "ours:") and k != mode + "ours:baseline":
+            v["speedup_vs_ours_unfused"] = round(ours["ms_per_step"] / v["ms_per_step"], 4)
         lb = row.get(mode + "fwd+bwd only (no update: lower bound)")
         if base and lb and k.startswith(mode + "ours:"):
             phase = base["ms_per_step"] - lb["ms_per_step"]
             if phase > 0:
                 v["unfused_update_phase_hidden"] = round((base["ms_per_step"] - v["ms_per_step"]) / phase, 3)
+
+
+def _headline_name(args) -> str:
+    if args.schedule == "baseline":
+        return "ours:baseline"
+    if args.schedule == "forward-fusion":
+        return f"ours:forward-fusion(bucket={_kname(args.ff_bucket_elems)})"
+    return f"ours:backward-fusion(w={args.workers},bucket={_kname(args.bucket_elems)})"
+
+
+def _kname(n: int) -> str:
+    if n <= 0:
+        return "per-layer"
+    return f"{n >> 20}M" if n % (1 << 20) == 0 else f"{n >> 10}K"
+
+
+def headline_arms(args) -> list:
+    """The headline and its same-mode comparators (same graph / layout mode,
+    same model math), timed interleaved instance by instance:
+    (row name, make_runner keyword arguments)."""
+    arms = [(_headline_name(args), {})]
+    if args.schedule != "baseline":
+        arms.append(("ours:baseline", {"schedule": "baseline"}))
+    if args.schedule != "forward-fusion":
+        arms.append((f"ours:forward-fusion(bucket={_kname(1 << 18)})",
+                     {"schedule": "forward-fusion", "bucket_elems": 1 << 18}))
+    if args.schedule != "backward-fusion":
+        arms.append((f"ours:backward-fusion(w=2,bucket={_kname(args.bucket_elems)})",
+                     {"schedule": "backward-fusion", "workers": 2,
+                      "bucket_elems": args.bucket_elems}))
+    arms += [("torch.optim.SGD(foreach)", {"schedule": "baseline", "opt_impl": "foreach"}),
+             ("torch.optim.SGD(fused)", {"schedule": "baseline", "opt_impl": "fused"}),
+             (FLOOR, {"schedule": "baseline", "opt_impl": "none"})]
+    return arms
+
+
+FLOOR = "fwd+bwd only (no update: lower bound)"
 
 
 def run_ours(args) -> dict:
@@ -709,157 +707,178 @@ def run_ours(args) -> dict:
     # between model instances and ~1 instance in 4 lands 5-8% off the others
     # (tools/cudnn_variance.py); with 0 every instance of every arm agrees
     torch.backends.cudnn.benchmark_limit = 0
-    # fp32 training on B200 the usual way: TF32 tensor cores for matmuls as
-    # well as convolutions (cuDNN's default), for every arm alike
-    torch.backends.cuda.matmul.allow_tf32 = True
+    # true fp32 (the reference's arithmetic): no TF32 tensor cores in any arm
+    # unless --tf32 1 asks for the (labelled) TF32 variant
+    torch.backends.cudnn.allow_tf32 = bool(args.tf32)
+    torch.backends.cuda.matmul.allow_tf32 = bool(args.tf32)
     peaks = load_peaks()
     args.world = dist.world
     args.dp = dist.world > 1 or args.force_dp
     flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=device)
     flush = flush_buf.zero_
 
-    # cuDNN picks per model instance; timings are stable within an instance but
-    # differ by up to ~7% between instances (both arms), so the headline is the
-    # median over --instances independently built instances, each timed for
-    # exactly K steps after W warm-up steps.
-    inst = []
+    # Every arm is built --instances times; the instances of all arms are
+    # interleaved (instance i of every arm, then instance i+1), each timed for
+    # exactly K steps after W warm-up steps; each row is the median over its
+    # instances.  cuDNN picks per model instance, and the GPU drifts between
+    # slow and fast windows, so interleaving keeps the
+    # fused/unfused comparison inside the same windows.
+    arms = headline_arms(args)
+    if args.headline_only:
+        arms = arms[:1]
+    times = {name: [] for name, _ in arms}
+    head = arms[0][0]
+    launches = 0
     dp_graph_error = None
     with Clocks(dist.local) as clk:
         for _ in range(args.instances):
-            try:
-                step, g, pol = make_runner(args, args.batch, args.schedule, device)
-            except Exception as e:  # noqa: BLE001
-                if not (args.dp and args.dp_graphs):
-                    raise
-                # data-parallel capture failed: measure the eager data-parallel step
-                args.dp_graphs = 0
-                dp_graph_error = f"{type(e).__name__}: {str(e).splitlines()[0][:160] if str(e) else ''}"
-                torch.cuda.synchronize()
-                step, g, pol = make_runner(args, args.batch, args.schedule, device)
-            n0 = _native.launch_count()
-            inst.append(timed(step, args.steps, args.warmup, dist, flush))
-            if hasattr(step, "native_launches"):   # CUDA graph: kernel nodes replayed per step
-                launches = step.native_launches * args.steps
-            else:
-                launches = (_native.launch_count() - n0) * args.steps // (args.steps + args.warmup)
-            del step, g, pol
-            torch.cuda.empty_cache()
-    ms = statistics.median(inst)
+            for name, kw in arms:
+                kw = dict(kw)
+                sched = kw.pop("schedule", args.schedule)
+                try:
+                    step, g, pol = make_runner(args, args.batch, sched, device, **kw)
+                except Exception as e:  # noqa: BLE001
+                    if not (args.dp and args.dp_graphs):
+                        raise
+                    # data-parallel capture failed: measure the eager data-parallel step
+                    args.dp_graphs = 0
+                    dp_graph_error = f"{type(e).__name__}: {str(e).splitlines()[0][:160] if str(e) else ''}"
+                    torch.cuda.synchronize()
+                    step, g, pol = make_runner(args, args.batch, sched, device, **kw)
+                n0 = _native.launch_count()
+                times[name].append(timed(step, args.steps, args.warmup, dist, flush))
+                if name == head:
+                    if hasattr(step, "native_launches"):   # CUDA graph: kernel nodes per replay
+                        launches = step.native_launches * args.steps
+                    else:
+                        launches = (_native.launch_count() - n0) * args.steps // (args.steps + args.warmup)
+                del step, g, pol
+                torch.cuda.empty_cache()
     clocks = clk.summary()
+    med = {k: statistics.median(v) for k, v in times.items()}
+    ms = med[head]
     value = dist.world * args.batch * 1e3 / ms
+    graphed = bool(args.graphs) and (not args.dp or bool(args.dp_graphs))
+    mode = ("graph" if graphed else "eager") + (", NHWC" if args.channels_last else "")
+    math = "fp32 (TF32 off)" if not args.tf32 else "fp32 weights, TF32 tensor cores"
+    if args.dp:
+        mode += f", data parallel over {args.dp_transport}"
+    workload = (f"C2 MobileNetV2 (10 classes) on synthetic 3x32x32, batch {args.batch}/GPU, "
+                f"SGD-momentum, {math}; {head}, {mode}")
+
+    def ratio(name):
+        return round(med[name] / ms, 4) if name in med else None
+
+    def med_ms(name):
+        return round(med[name], 4) if name in med else None
+
+    unfused_torch = "DDP + " if args.dp else ""
     res = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": dist.world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-           "data": "synthetic (x~N(0,1) [b,3,32,32], y~U{0..9}; random-init weights)",
-           "config": {"workload": WORKLOAD, "model": args.model, "batch_per_gpu": args.batch,
-                      "global_batch": args.batch * dist.world, "schedule": args.schedule,
-                      "workers": args.workers, "grad_reset": args.grad_reset,
-                      "bucket_elems": args.bucket_elems,
-                      "cuda_graph": bool(args.graphs) and (not args.dp or bool(args.dp_graphs)),
-                      "channels_last": bool(args.channels_last),
-                      "parallelism": f"dp{dist.world}",
-                      "dp_path": (("sharded fused update: per-bucket NCCL reduce-scatter -> update "
-                                   "-> all-gather" if args.dp_transport == "nccl" else
-                                   "fused peer-memory kernel per bucket (reduce-scatter + update + "
-                                   "all-gather in one kernel over symmetric memory)")
-                                  + "; unfused baseline DDP + torch.optim" if args.dp else None),
-                      "l2": "256 MiB buffer zeroed before every timed step (outside each step's event pair)",
-                      "model_math": ("fp32 parameters/activations; TF32 tensor cores for convolutions "
-                                     f"(cudnn.allow_tf32={torch.backends.cudnn.allow_tf32}) and matmuls "
-                                     f"(matmul.allow_tf32={torch.backends.cuda.matmul.allow_tf32}); "
-                                     "optimizer update exact fp32 (reference arithmetic)")},
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "f32" if not args.tf32 else "tf32",
+           "data": "synthetic x~N(0,1), y~U{0..9}; random-init weights",
+           "config": {"workload": workload, "global_batch": args.batch * dist.world,
+                      "parallelism": f"dp{dist.world}", "instances": args.instances,
+                      "l2": "256 MiB flush before every timed step, outside its events"},
+           "unfused": {"ours_baseline_ms": med_ms("ours:baseline"),
+                       "torch_foreach_ms": med_ms("torch.optim.SGD(foreach)"),
+                       "torch_fused_ms": med_ms("torch.optim.SGD(fused)"),
+                       "fwd_bwd_floor_ms": med_ms(FLOOR),
+                       "speedup_vs_ours_unfused": ratio("ours:baseline"),
+                       "speedup_vs_torch_foreach": ratio("torch.optim.SGD(foreach)"),
+                       "speedup_vs_torch_fused": ratio("torch.optim.SGD(fused)"),
+                       "torch_arm": unfused_torch + "torch.optim, same mode"},
            "gpu_launches": int(launches)}
-    res["config"]["instances_ms_per_step"] = [round(t, 4) for t in inst]
+    extras = {"rows": {k: {"ms_per_step": round(med[k], 4),
+                           "images_per_s": round(dist.world * args.batch * 1e3 / med[k], 1),
+                           "instances_ms": [round(t, 4) for t in v]} for k, v in times.items()},
+              "mode": mode, "model_math": math,
+              "torch_backends": {"cudnn.allow_tf32": torch.backends.cudnn.allow_tf32,
+                                 "matmul.allow_tf32": torch.backends.cuda.matmul.allow_tf32,
+                                 "cudnn.benchmark_limit": 0}}
     if dp_graph_error:
-        res["config"]["dp_graph_capture_failed"] = dp_graph_error
-    if not args.no_extras:
-        sched, failed = {}, {}
-        for b in [args.batch] + [int(x) for x in args.sweep.split(",") if x.strip()]:
-            row = {}
-            for name, sch, w, gr, opt, be, gph, cl in _variants_c2(2 if args.dp else 1, bool(args.dp_graphs)):
-                if b != args.batch and name not in SWEEP_ROWS:
-                    continue
-                ts = []
-                try:
-                    for _ in range(args.instances if name in KEY_ROWS else 1):
-                        st, *_ = make_runner(args, b, sch, device, workers=w, grad_reset=gr,
-                                             opt_impl=opt, bucket_elems=be, graphed=gph,
-                                             channels_last=cl)
-                        ts.append(timed(st, args.steps, args.warmup, dist, flush))
-                        del st
-                        torch.cuda.empty_cache()
-                except Exception as e:  # noqa: BLE001 -- report, keep the other rows
-                    failed[f"{b}:{name}"] = f"{type(e).__name__}: {str(e).splitlines()[0][:160] if str(e) else ''}"
-                    torch.cuda.synchronize()
-                    continue
-                t = statistics.median(ts)
-                row[name] = {"ms_per_step": round(t, 4), "images_per_s": round(dist.world * b * 1e3 / t, 1)}
-                if len(ts) > 1:
-                    row[name]["instances_ms"] = [round(x, 4) for x in ts]
-            _speedups(row)
-            sched[str(b)] = row
-        res["schedules"] = sched
-        if failed:
-            res["failed_rows"] = failed
-        row = sched.get(str(args.batch), {})
-        headline_graphed = bool(args.graphs) and (not args.dp or bool(args.dp_graphs))
-        mode = (("cl:" if args.channels_last else "")
-                + ("graph:" if headline_graphed else ""))
-        same = row.get(mode + "torch.optim.SGD(foreach)") or row.get("torch.optim.SGD(foreach)")
-        eager = row.get("torch.optim.SGD(foreach)")
-        lb = row.get(mode + "fwd+bwd only (no update: lower bound)")
-        res["vs_unfused_torch"] = {
-            "mode": mode or "eager",
-            "torch_foreach_ms": same["ms_per_step"] if same else None,
-            "speedup": round(same["ms_per_step"] / ms, 4) if same else None,
-            "fwd_bwd_only_ms": lb["ms_per_step"] if lb else None,
-            "speedup_vs_eager_torch_foreach": round(eager["ms_per_step"] / ms, 4) if eager else None}
-        for wl, key in (("c1", "c1_resnet18_sgdm"), ("c3", "c3_vgg16_adam"),
-                        ("c4", "c4_resnet50_bf16_adamw"), ("c5", "c5_bert_base_adamw")):
-            if wl in args.extras.split(","):
-                res[key] = run_extra(args, wl, device, dist, flush)
-        res["e2e"] = e2e(args, device, dist, flush)
-        # the kernel's own duration is a per-GPU quantity: measured on this
-        # GPU's single-process engine whatever the world size
-        world, dp, args.world, args.dp = args.world, args.dp, 1, False
-        try:
-            ins = measure_in_situ(args, device, peaks, 5)
-            live = measure_in_graph(args, device, peaks, flush) if args.graphs else None
-        finally:
-            args.world, args.dp = world, dp
+        extras["dp_graph_capture_failed"] = dp_graph_error
+    if args.headline_only:
+        res["clocks"] = clocks
+        dist.close()
+        return res
+    res["e2e"] = e2e(args, device, dist, flush)
+    extras["e2e_instances"] = res["e2e"].pop("instances")
+    # the kernel's own duration is a per-GPU quantity: measured on this GPU's
+    # single-process engine whatever the world size
+    world, dp, args.world, args.dp = args.world, args.dp, 1, False
+    try:
+        live = measure_in_graph(args, device, peaks, flush) if args.graphs else None
+        ins = measure_in_situ(args, device, peaks, 5)
+    finally:
+        args.world, args.dp = world, dp
+    tr = ncu_traffic("c2_backward_fusion_buckets")
+    prim = live or ins
+    res["roofline"] = {"bound": "hbm", "kernel": "mt_step_kernel",
+                       "achieved": round(prim["achieved_gbs"], 1), "peak": peaks["hbm_gbs"],
+                       "unit": "GB/s", "frac": round(prim["frac"], 4),
+                       "traffic": (tr or {}).get("dram_bytes_per_launch"),
+                       "bytes_per_launch": round(prim["avg_bytes"]),
+                       "us_per_launch": round(prim["avg_us"], 3),
+                       "launches_per_step": prim["launches_per_step"]}
+    extras["roofline"] = {
+        "method": ("CUDA events captured as event-record nodes around each update launch of the "
+                   "headline graph, read after every replay (live, beside the backward)")
+        if live else "one iteration's launches replayed back to back",
+        "peak_source": peaks["source"], "traffic_source": (tr or {}).get("source"),
+        "in_graph_live": live, "replayed_back_to_back": ins}
+    if args.sweep:
+        extras["batch_sweep"] = run_sweep(args, device, dist, flush)
+    for wl in [w for w in args.extras.split(",") if w.strip()]:
+        extras[wl] = run_extra(args, wl, device, dist, flush)
+    if args.standalone:
         std = measure_update_kernel(args, device, peaks)
-        tr = ncu_traffic("c2_backward_fusion_buckets")
-        prim = live or ins
-        res["roofline"] = {"bound": "hbm", "kernel": "mt_step_kernel (backward-fusion, side stream)",
-                           "achieved": round(prim["achieved_gbs"], 1), "peak": peaks["hbm_gbs"],
-                           "unit": "GB/s", "frac": round(prim["frac"], 4),
-                           "method": ("CUDA events captured as event-record nodes around each "
-                                      "update launch, read after every replay of the headline "
-                                      "graph (live, beside the backward)") if live else
-                                     "one iteration's launches replayed back to back",
-                           "in_graph_live": ({"avg_bytes": round(live["avg_bytes"]),
-                                              "avg_us": round(live["avg_us"], 3),
-                                              "launches_per_step": live["launches_per_step"]}
-                                             if live else None),
-                           "traffic": (tr or {}).get("dram_bytes_per_launch"),
-                           "traffic_source": (tr or {}).get("source"),
-                           "peak_source": peaks["source"],
-                           "replayed_back_to_back": {
-                               "avg_bytes": round(ins["avg_bytes"]), "avg_us": round(ins["avg_us"], 3),
-                               "launches_per_step": ins["launches_per_step"],
-                               "frac": round(ins["frac"], 4),
-                               "method": "one iteration's launches replayed back to back on their "
-                                         "stream after an eager step, one event pair"},
-                           "live_eager_beside_backward": ins["live_beside_backward"],
-                           "standalone_single_launch": std}
-        if dist.rank == 0 and dist.world == 1:
-            res["cpu_baseline"] = cpu_baseline(args, args.cpu_iters)
-            res["cpu_update_baseline"] = cpu_update_baseline(std)
-            from oracle import timing
-            res["cpu_harness_baseline"] = dict(timing.reference_harness_breakdown(), kind="port")
+        extras["standalone_single_launch"] = std
+    if dist.rank == 0 and dist.world == 1:
+        res["cpu_baseline"] = cpu_baseline(args)
+        if args.standalone:
+            extras["cpu_update_baseline"] = cpu_update_baseline(std)
     res["clocks"] = clocks
     dist.close()
+    if dist.rank == 0 and args.extras_out:
+        out = Path(args.extras_out)
+        out.parent.mkdir(parents=True, exist_ok=True)
+        extras["headline_line"] = res
+        out.write_text(json.dumps(extras, indent=1))
+        res["extras"] = str(out)
     return res
+
+
+def run_sweep(args, device, dist, flush) -> dict:
+    """Batch sweep (C2: per-GPU batch 32..512) of the headline, ours unfused
+    and torch foreach, interleaved per instance."""
+    import torch
+    out = {}
+    arms = [a for a in headline_arms(args)
+            if a[0] in (_headline_name(args), "ours:baseline", "torch.optim.SGD(foreach)", FLOOR)]
+    for b in [int(x) for x in args.sweep.split(",") if x.strip()]:
+        times = {n: [] for n, _ in arms}
+        for _ in range(args.instances):
+            for name, kw in arms:
+                kw = dict(kw)
+                sched = kw.pop("schedule", args.schedule)
+                st, *_ = make_runner(args, b, sched, device, **kw)
+                times[name].append(timed(st, args.steps, args.warmup, dist, flush))
+                del st
+                torch.cuda.empty_cache()
+        row = {}
+        for n, v in times.items():
+            t = statistics.median(v)
+            row[n] = {"ms_per_step": round(t, 4), "images_per_s": round(dist.world * b * 1e3 / t, 1),
+                      "instances_ms": [round(x, 4) for x in v]}
+        h = row[_headline_name(args)]["ms_per_step"]
+        for n in ("ours:baseline", "torch.optim.SGD(foreach)"):
+            if n in row:
+                row[_headline_name(args)][f"speedup_vs_{n}"] = round(row[n]["ms_per_step"] / h, 4)
+        out[str(b)] = row
+    return out
+
 
 
 OWN_LB = "fwd+bwd only (bf16 module as ours: lower bound for ours)"
@@ -868,37 +887,24 @@ OWN_LB = "fwd+bwd only (bf16 module as ours: lower bound for ours)"
 def _variants_extra(wl: str):
     """(name, schedule, workers, torch optimizer, bucket, CUDA graph) for the extras."""
     opt = WORKLOADS[wl]["torch"][0]
-    LB = "fwd+bwd only (no update: lower bound)"
-    v = [(f"torch.optim.{opt}(foreach)", "baseline", None, "foreach", 0, False),
-         (f"torch.optim.{opt}(fused)", "baseline", None, "fused", 0, False),
-         (LB, "baseline", None, "none", 0, False),
-         ("ours:baseline", "baseline", None, None, 0, False),
-         ("ours:forward-fusion(per-layer)", "forward-fusion", None, None, 0, False),
-         ("ours:backward-fusion(w=2,per-layer)", "backward-fusion", 2, None, 0, False),
-         ("ours:backward-fusion(w=2,per-layer,default-prio)", "backward-fusion", -2, None, 0, False),
-         # inline on the autograd stream: each update right behind its layer's backward,
-         # gradients (and the weights dgrad just read) still in L2 -- the paper's locality
-         ("ours:backward-fusion(w=1,per-layer)", "backward-fusion", 1, None, 0, False)]
-    if WORKLOADS[wl].get("mixed"):
-        v.append((OWN_LB, "baseline", None, "none-mixed", 0, False))
-    if wl == "c3":
-        v.append(("ours:backward-fusion(w=2,per-layer,capped)", "backward-fusion", -1, None, 0, False))
-    else:
-        v.append(("ours:forward-fusion(bucket=1M)", "forward-fusion", None, None, 1 << 20, False))
-        v.append(("ours:forward-fusion(bucket=1M,prefetch)", "forward-fusion", 2, None, 1 << 20, False))
-        v.append(("ours:backward-fusion(w=2,bucket=1M)", "backward-fusion", 2, None, 1 << 20, False))
-    # the same iteration captured as one CUDA graph (Adam/AdamW replay through
-    # the device-side step index; torch's Adam with capturable=True)
-    v += [(f"graph:torch.optim.{opt}(foreach)", "baseline", None, "foreach", 0, True),
-          (f"graph:torch.optim.{opt}(fused)", "baseline", None, "fused", 0, True),
-          ("graph:" + LB, "baseline", None, "none", 0, True),
-          ("graph:ours:baseline", "baseline", None, None, 0, True),
-          ("graph:ours:forward-fusion(bucket=1M)", "forward-fusion", None, None, 1 << 20, True),
-          ("graph:ours:forward-fusion(bucket=1M,prefetch)", "forward-fusion", 2, None, 1 << 20, True),
-          ("graph:ours:backward-fusion(w=2,bucket=1M)", "backward-fusion", 2, None, 1 << 20, True),
-          ("graph:ours:backward-fusion(w=1,per-layer)", "backward-fusion", 1, None, 0, True)]
-    if WORKLOADS[wl].get("mixed"):
-        v.append(("graph:" + OWN_LB, "baseline", None, "none-mixed", 0, True))
+    LB = FLOOR
+    v = []
+    for gph, pre in ((False, ""), (True, "graph:")):
+        # (graph mode: Adam/AdamW replay through the device-side step index;
+        # torch's Adam with capturable=True)
+        v += [(f"{pre}torch.optim.{opt}(foreach)", "baseline", None, "foreach", 0, gph),
+              (f"{pre}torch.optim.{opt}(fused)", "baseline", None, "fused", 0, gph),
+              (pre + LB, "baseline", None, "none", 0, gph),
+              (pre + "ours:baseline", "baseline", None, None, 0, gph),
+              (pre + "ours:forward-fusion(per-layer)", "forward-fusion", None, None, 0, gph),
+              (pre + "ours:forward-fusion(bucket=1M)", "forward-fusion", None, None, 1 << 20, gph),
+              (pre + "ours:backward-fusion(w=2,per-layer)", "backward-fusion", 2, None, 0, gph),
+              (pre + "ours:backward-fusion(w=2,bucket=1M)", "backward-fusion", 2, None, 1 << 20, gph),
+              # inline on the autograd stream: each update right behind its layer's backward,
+              # gradients (and the weights dgrad just read) still in L2 -- the paper's locality
+              (pre + "ours:backward-fusion(w=1,per-layer)", "backward-fusion", 1, None, 0, gph)]
+        if WORKLOADS[wl].get("mixed"):
+            v.append((pre + OWN_LB, "baseline", None, "none-mixed", 0, gph))
     return v
 
 
@@ -906,29 +912,38 @@ def run_extra(args, wl: str, device, dist, flush) -> dict:
     """One of BASELINE.json's other configs on this GPU, eager and captured as
     CUDA graphs: C1 ResNet-18/CIFAR SGD-momentum, C3 VGG-16 Adam (the
     update-bound case), C4 ResNet-50 bf16 + fp32 masters AdamW, C5 BERT-base
-    AdamW."""
+    AdamW.  Every row is built --instances times, instances interleaved across
+    rows (instance i of every row, then i+1); each row is the median."""
     import torch
     b = WORKLOADS[wl]["batch"]
-    steps, warm = max(args.steps // 3, 5), 3
-    row, failed = {}, {}
-    for name, sch, w, opt, be, gph in _variants_extra(wl):
-        if gph and args.dp and not args.dp_graphs:
-            continue
-        try:
-            st, *_ = make_runner(args, b, sch, device, workers=w, opt_impl=opt, bucket_elems=be,
-                                 graphed=gph, workload=wl, channels_last=wl in ("c4",))
-            t = timed(st, steps, warm, dist, flush)
-        except Exception as e:  # noqa: BLE001 -- report, keep the other rows
-            failed[name] = f"{type(e).__name__}: {str(e).splitlines()[0][:160] if str(e) else ''}"
-            torch.cuda.synchronize()
-            continue
-        row[name] = {"ms_per_step": round(t, 3), "images_per_s": round(dist.world * b * 1e3 / t, 1)}
-        del st
-        torch.cuda.empty_cache()
+    steps, warm = max(args.steps // 2, 10), 3
+    variants = [v for v in _variants_extra(wl) if not (v[5] and args.dp and not args.dp_graphs)]
+    times, failed = {v[0]: [] for v in variants}, {}
+    for _ in range(args.instances):
+        for name, sch, w, opt, be, gph in variants:
+            if name in failed:
+                continue
+            try:
+                st, *_ = make_runner(args, b, sch, device, workers=w, opt_impl=opt, bucket_elems=be,
+                                     graphed=gph, workload=wl, channels_last=wl in ("c4",))
+                times[name].append(timed(st, steps, warm, dist, flush))
+            except Exception as e:  # noqa: BLE001 -- report, keep the other rows
+                failed[name] = f"{type(e).__name__}: {str(e).splitlines()[0][:160] if str(e) else ''}"
+                torch.cuda.synchronize()
+                continue
+            del st
+            torch.cuda.empty_cache()
+    row = {}
+    for name, ts in times.items():
+        if ts:
+            t = statistics.median(ts)
+            row[name] = {"ms_per_step": round(t, 3), "images_per_s": round(dist.world * b * 1e3 / t, 1),
+                         "instances_ms": [round(x, 3) for x in ts]}
     _speedups(row)
-    out = {"workload": WORKLOADS[wl]["desc"], "batch_per_gpu": b, "steps": steps, "warmup": warm}
+    out = {"workload": WORKLOADS[wl]["desc"], "batch_per_gpu": b, "steps": steps, "warmup": warm,
+           "instances": args.instances}
     for mode in ("", "graph:"):
-        lb = row.pop(mode + "fwd+bwd only (no update: lower bound)", None)
+        lb = row.pop(mode + FLOOR, None)
         own = row.pop(mode + OWN_LB, None)
         key = mode.rstrip(":") or "eager"
         if lb is not None:
@@ -1036,17 +1051,20 @@ def run_reference(args) -> dict | None:
         return None
     from oracle import timing
     kw = dict(eta=0.1, alpha=0.9, weight_decay=5e-4)
-    timing.cpu_training_sample(args.model, args.batch, 1, "sgd-momentum", kw)  # warm-up
-    r = timing.cpu_training_sample(args.model, args.batch, max(args.steps, 1), "sgd-momentum", kw)
+    r = timing.cpu_training_sample(args.model, args.batch, max(args.steps, 1), "sgd-momentum", kw,
+                                   warmup=max(args.warmup, 1))
     v = round(r["images_per_s"], 3)
     return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 0,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(r["ms_per_iter"], 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic", "config": {"workload": WORKLOAD, "model": args.model,
-                                             "batch_per_gpu": args.batch, "schedule": "baseline"},
+            "data": "synthetic x~N(0,1), y~U{0..9}; random-init weights",
+            "config": {"workload": (f"C2 MobileNetV2 (10 classes) on synthetic 3x32x32, batch "
+                                    f"{args.batch}, SGD-momentum, fp32; reference CPU path "
+                                    f"(unfused: forward, backward, per-parameter update)"),
+                       "global_batch": args.batch, "parallelism": "cpu"},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": r["threads"], "kind": "port",
-                             "sample": (f"each step: one iteration at batch {args.batch}, "
-                                        f"torch-CPU fwd/bwd on {r['threads']} threads + the "
+                             "sample": (f"each step: one iteration at batch {args.batch}, pinned "
+                                        f"to {r['threads']} cores: torch-CPU fwd/bwd + the "
                                         f"reference update (numpy oracle port, 1 thread)")},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
@@ -1058,7 +1076,10 @@ def main(argv=None):
     else:
         res = run_ours(args)
     if res is not None and int(os.environ.get("RANK", "0")) == 0:
-        print(json.dumps(res), flush=True)
+        line = json.dumps(res, separators=(",", ":"))
+        if len(line) > 2048:
+            print(f"bench: result line is {len(line)} bytes (> 2 KB)", file=sys.stderr)
+        print(line, flush=True)
 
 
 if __name__ == "__main__":

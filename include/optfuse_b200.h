@@ -42,7 +42,9 @@
 extern "C" {
 #endif
 
-#define OF_ABI_VERSION 2
+/* ABI 3: grad_scale_dev of of_policy_step_mt is untyped (f32, or f64 with
+ * OF_FLAG_SCALE_F64); of_mc_bucket carries dtypes. */
+#define OF_ABI_VERSION 3
 
 typedef enum of_status {
   OF_OK = 0,
@@ -74,6 +76,7 @@ typedef enum of_kind {
 #define OF_FLAG_ZERO_GRAD 0x1u   /* write grad = 0 after reading it (optim.py:111) */
 #define OF_FLAG_SHADOW_BF16 0x2u /* also write a bf16 copy of the new parameter */
 #define OF_FLAG_DEVICE_STEP 0x4u /* read the step index on the device (see of_hparams) */
+#define OF_FLAG_SCALE_F64 0x8u   /* grad_scale_dev points to a double (ABI 3) */
 
 /* Hyper-parameters of one policy step (optim.py:42-51).  Scalars are the
  * Python doubles; the library rounds them to the tensor precision. */
@@ -133,18 +136,21 @@ uint64_t of_launch_count(void);
 
 /* One policy step over every tensor of `list` (OptimizerPolicy.step,
  * optim.py:74-115, applied to several parameters in one multi-tensor launch).
- * grad_scale_dev: NULL, or a device f32 scalar multiplied into every gradient
- * before the update (the global-norm clip factor, optim.py:170). */
+ * grad_scale_dev: NULL, or a device scalar multiplied into every gradient
+ * before the update (the global-norm clip factor, optim.py:170): an f32 value,
+ * or with OF_FLAG_SCALE_F64 an f64 value rounded once to the parameter
+ * precision -- numpy scales f64 gradients by the double factor itself, f32
+ * gradients by its f32 rounding, so f64 lists pass the double. */
 int of_policy_step_mt(const of_tensor_list* list, const of_hparams* hp,
-                      const float* grad_scale_dev, uint32_t flags, void* stream);
+                      const void* grad_scale_dev, uint32_t flags, void* stream);
 
 /* Convenience wrappers with the kind fixed (same semantics). */
 int of_sgdm_mt(const of_tensor_list* list, double eta, double alpha, double weight_decay,
-               const float* grad_scale_dev, uint32_t flags, void* stream);
+               const void* grad_scale_dev, uint32_t flags, void* stream);
 int of_adam_mt(const of_tensor_list* list, double eta, double beta1, double beta2,
                double epsilon, double weight_decay, double bias_correction1,
                double bias_correction2, int decoupled_weight_decay,
-               const float* grad_scale_dev, uint32_t flags, void* stream);
+               const void* grad_scale_dev, uint32_t flags, void* stream);
 
 /* *step_offset_dev += delta on `stream` (one thread): the first node of a
  * captured iteration, advancing the device step index of OF_FLAG_DEVICE_STEP
@@ -183,7 +189,9 @@ typedef struct of_peer_bucket {
 int of_dp_step_peer(const of_peer_bucket* bucket, const of_hparams* hp,
                     const float* grad_scale_dev, uint32_t flags, void* stream);
 
-/* The same bucket step over NVLink SHARP (NVLS) multicast: the shard's gradient is
+/* EXPERIMENTAL (not used by the data-parallel host layer; its numerics have
+ * not run on a multi-GPU box yet).
+ * The same bucket step over NVLink SHARP (NVLS) multicast: the shard's gradient is
  * read once through the multicast address with an in-switch sum
  * (multimem.ld_reduce), the new parameters and the zeroed gradient are written
  * once to every peer through multicast stores (multimem.st).  fp32 only.  The
@@ -193,6 +201,8 @@ int of_dp_step_peer(const of_peer_bucket* bucket, const of_hparams* hp,
 typedef struct of_mc_bucket {
   int32_t world;           /* W, 1 .. OF_MAX_PEERS */
   int32_t rank;
+  int32_t param_dtype;     /* must be OF_F32 (anything else: OF_ERR_UNSUPPORTED) */
+  int32_t grad_dtype;      /* must be OF_F32 */
   void* mc_grad;           /* multicast address of the flat gradient buffer */
   void* mc_param;          /* multicast address of the flat parameter buffer */
   void* local_param;       /* this rank's flat parameter buffer (unicast) */

@@ -25,41 +25,75 @@ def host_cores() -> int:
         return os.cpu_count() or 1
 
 
+def _network(model_name: str):
+    """The benchmark network, built here from torchvision (the reference arm
+    must not touch the product package): CIFAR-shaped MobileNetV2 / ResNet-18."""
+    import torch
+    import torchvision
+    if model_name == "mobilenet_v2_cifar":
+        return torchvision.models.mobilenet_v2(num_classes=10), (3, 32, 32), 10
+    if model_name == "resnet18_cifar":
+        m = torchvision.models.resnet18(num_classes=10)
+        m.conv1 = torch.nn.Conv2d(3, 64, kernel_size=3, stride=1, padding=1, bias=False)
+        m.maxpool = torch.nn.Identity()
+        return m, (3, 32, 32), 10
+    raise ValueError(f"no CPU baseline for {model_name!r}")
+
+
+def _batch(shape, classes: int, batch: int, seed: int):
+    """x ~ N(0, 1), y ~ U{0..classes-1} from a CPU generator (the GPU arm's
+    synthetic_batch draws the same way)."""
+    import torch
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    return torch.randn((batch,) + shape, generator=g), torch.randint(0, classes, (batch,), generator=g)
+
+
 def cpu_training_sample(model_name: str, batch: int, iters: int, kind: str, hp: dict,
-                        threads: int | None = None, seed: int = 0) -> dict:
-    """``iters`` iterations of forward/backward (torch CPU) + the reference
-    update (numpy oracle) on ``model_name``; returns timings and images/s."""
+                        threads: int | None = None, seed: int = 0, warmup: int = 1) -> dict:
+    """``warmup`` + ``iters`` iterations of forward/backward (torch CPU) + the
+    reference update (numpy oracle, one thread) on ``model_name``, pinned to
+    the first ``threads`` allowed cores (all of them by default); returns the
+    timed iterations' means and images/s."""
     import torch
     import torch.nn.functional as F
 
-    from paper_2104_00237_b200.models import CLASSIFIERS, synthetic_batch
-
+    allowed = sorted(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else None
     threads = threads or host_cores()
+    if allowed is not None:
+        os.sched_setaffinity(0, allowed[:threads])
+    prev_threads = torch.get_num_threads()
     torch.set_num_threads(threads)
-    torch.manual_seed(seed)
-    net = CLASSIFIERS[model_name][0]()
-    x, y = synthetic_batch(model_name, batch, device="cpu", seed=seed)
-    params = [p for p in net.parameters() if p.requires_grad]
-    h = optim_ref.Hyper(kind=kind, **hp)
-    slots = [dict() for _ in params]
-    fb, upd = [], []
-    for t in range(1, iters + 1):
-        t0 = time.perf_counter()
-        loss = F.cross_entropy(net(x), y)
-        loss.backward()
-        t1 = time.perf_counter()
-        for p, sl in zip(reversed(params), reversed(slots)):
-            theta = p.detach().numpy().reshape(-1)   # shares storage with the torch parameter
-            grad = p.grad.numpy().reshape(-1)
-            optim_ref.step(kind, h, theta, grad, sl, t)
-        t2 = time.perf_counter()
-        fb.append(t1 - t0)
-        upd.append(t2 - t1)
+    try:
+        torch.manual_seed(seed)
+        net, shape, classes = _network(model_name)
+        x, y = _batch(shape, classes, batch, seed)
+        params = [p for p in net.parameters() if p.requires_grad]
+        h = optim_ref.Hyper(kind=kind, **hp)
+        slots = [dict() for _ in params]
+        fb, upd = [], []
+        for t in range(1, warmup + iters + 1):
+            t0 = time.perf_counter()
+            loss = F.cross_entropy(net(x), y)
+            loss.backward()
+            t1 = time.perf_counter()
+            for p, sl in zip(reversed(params), reversed(slots)):
+                theta = p.detach().numpy().reshape(-1)   # shares storage with the torch parameter
+                grad = p.grad.numpy().reshape(-1)
+                optim_ref.step(kind, h, theta, grad, sl, t)
+            t2 = time.perf_counter()
+            if t > warmup:
+                fb.append(t1 - t0)
+                upd.append(t2 - t1)
+    finally:
+        torch.set_num_threads(prev_threads)
+        if allowed is not None:
+            os.sched_setaffinity(0, allowed)
     n_elem = sum(p.numel() for p in params)
     per_iter = float(np.mean(fb) + np.mean(upd))
     return {"images_per_s": batch / per_iter, "ms_per_iter": per_iter * 1e3,
             "fwd_bwd_ms": float(np.mean(fb)) * 1e3, "update_ms": float(np.mean(upd)) * 1e3,
-            "update_elems": n_elem, "threads": threads, "batch": batch, "iters": iters}
+            "update_elems": n_elem, "threads": threads, "batch": batch, "iters": iters,
+            "warmup": warmup}
 
 
 def reference_update_rate(kind: str, hp: dict, elems: int = 1 << 22, reps: int = 3) -> dict:

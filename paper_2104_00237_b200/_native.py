@@ -21,7 +21,8 @@ OF_F32, OF_F64, OF_BF16 = 0, 1, 2
 OF_FLAG_ZERO_GRAD = 0x1
 OF_FLAG_SHADOW_BF16 = 0x2
 OF_FLAG_DEVICE_STEP = 0x4
-ABI_VERSION = 2
+OF_FLAG_SCALE_F64 = 0x8
+ABI_VERSION = 3
 
 # of_kind (optim.py:22 minus newton, plus adamw)
 KIND_CODES = {"sgd": 0, "sgd-momentum": 1, "adagrad": 2, "rmsprop": 3, "adadelta": 4,
@@ -67,6 +68,7 @@ class OfPeerBucket(ctypes.Structure):
 
 class OfMcBucket(ctypes.Structure):
     _fields_ = [("world", ctypes.c_int32), ("rank", ctypes.c_int32),
+                ("param_dtype", ctypes.c_int32), ("grad_dtype", ctypes.c_int32),
                 ("mc_grad", _vp), ("mc_param", _vp), ("local_param", _vp),
                 ("state0", _vp), ("state1", _vp),
                 ("shard_begin", ctypes.c_int64), ("shard_len", ctypes.c_int64)]
@@ -90,6 +92,10 @@ def lib():
     except OSError as e:
         raise NativeLibraryError(f"cannot load {path}: {e}") from e
     so.of_abi_version.restype = ctypes.c_int
+    # version first: a stale library must fail here, not on a missing symbol
+    if so.of_abi_version() != ABI_VERSION:
+        raise NativeLibraryError(f"{path}: ABI version {so.of_abi_version()} != {ABI_VERSION} "
+                                 "(stale build: rerun __graft_entry__.build())")
     so.of_status_string.restype = ctypes.c_char_p
     so.of_status_string.argtypes = [ctypes.c_int]
     so.of_last_error.restype = ctypes.c_char_p
@@ -122,9 +128,6 @@ def lib():
                                 ctypes.c_int, _vp]
     so.of_clip_coef.restype = ctypes.c_int
     so.of_clip_coef.argtypes = [_vp, ctypes.c_double, _vp, _vp, _vp]
-    if so.of_abi_version() != ABI_VERSION:
-        raise NativeLibraryError(f"{path}: ABI version {so.of_abi_version()} != {ABI_VERSION} "
-                                 "(stale build: rerun __graft_entry__.build())")
     _lib = so
     return so
 

@@ -518,8 +518,10 @@ class Engine : public std::enable_shared_from_this<Engine> {
       cuda_check(cudaEventCreate(&b), "cudaEventCreate");
       record_timing(a, s);
     }
-    const float* gs = gscale_.defined() ? gscale_.data_ptr<float>() : nullptr;
-    const int st = of_policy_step_mt(&G.list, &hp_, gs, flags_, s);
+    const void* gs = gscale_.defined() ? gscale_.data_ptr() : nullptr;
+    const uint32_t fl = flags_ | (gscale_.defined() && gscale_.scalar_type() == at::kDouble
+                                      ? OF_FLAG_SCALE_F64 : 0u);
+    const int st = of_policy_step_mt(&G.list, &hp_, gs, fl, s);
     if (st != OF_OK)
       throw std::runtime_error(std::string("of_policy_step_mt: ") + of_status_string(st) + " (" +
                                of_last_error() + ")");

@@ -75,15 +75,6 @@ int check_launch(const char* what) {
   return OF_OK;
 }
 
-// OPTFUSE_TMA=1 selects the TMA-staged kernel for large fp32 launches (read once).
-bool use_tma() {
-  static const bool on = [] {
-    const char* e = std::getenv("OPTFUSE_TMA");
-    return e != nullptr && e[0] == '1';
-  }();
-  return on;
-}
-
 int sm_count() {
   static int cache[64] = {0};
   int dev = 0;
@@ -350,6 +341,17 @@ template <class P, class V> __device__ __forceinline__ void st4s(P* p, const V (
 #endif
 
 template <class T> __device__ __forceinline__ T ld1(const T* p) { return *p; }
+
+// The gradient scale (global-norm clip factor, optim.py:170): an f32 device
+// scalar, or with OF_FLAG_SCALE_F64 the f64 factor itself, rounded once to T
+// (numpy multiplies an f64 gradient by the Python-double factor, an f32 one by
+// its f32 rounding).
+template <class T>
+__device__ __forceinline__ T load_scale(const void* gscale, uint32_t flags) {
+  if (gscale == nullptr) return T(1);
+  if (flags & OF_FLAG_SCALE_F64) return static_cast<T>(*static_cast<const double*>(gscale));
+  return static_cast<T>(*static_cast<const float*>(gscale));
+}
 __device__ __forceinline__ float ld1(const __nv_bfloat16* p) { return __bfloat162float(*p); }
 template <class G> __device__ __forceinline__ void st1_zero(G* p) { *p = G(0); }
 __device__ __forceinline__ void st1_zero(__nv_bfloat16* p) { *p = __float2bfloat16_rn(0.f); }
@@ -382,7 +384,7 @@ template <> struct Tune<__nv_bfloat16> {
 template <class Op, class T, class G, int CAP, int UNR>
 __global__ void __launch_bounds__(kThreads, Tune<G>::kMinBlocks)
 mt_step_kernel(const __grid_constant__ MTParams<CAP> mp, const Op op_in,
-               const float* __restrict__ gscale, uint32_t flags, const StepSrc step) {
+               const void* __restrict__ gscale, uint32_t flags, const StepSrc step) {
   using GV = typename GradVal<G>::type;
   Op op = op_in;
   if (step.offset != nullptr) {  // OF_FLAG_DEVICE_STEP: this replay's step index
@@ -397,7 +399,7 @@ mt_step_kernel(const __grid_constant__ MTParams<CAP> mp, const Op op_in,
   const bool zero_grad = (flags & OF_FLAG_ZERO_GRAD) != 0;
   const bool shadow = (flags & OF_FLAG_SHADOW_BF16) != 0;
   const bool has_scale = gscale != nullptr;
-  const T scale = has_scale ? T(*gscale) : T(1);
+  const T scale = load_scale<T>(gscale, flags);
   int ti = 0;
   for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
     ti = find_tensor(mp, ti, tile);
@@ -462,186 +464,6 @@ mt_step_kernel(const __grid_constant__ MTParams<CAP> mp, const Op op_in,
       if (Op::kSlots >= 2) s1[e] = b;
       if (zero_grad) st1_zero(g + e);
       if (shadow) sh[e] = __float2bfloat16_rn(static_cast<float>(pv));
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// TMA-staged variant (experimental, OPTFUSE_TMA=1): the input streams of each
-// 2048-element tile (theta, grad, history) arrive in shared memory by bulk
-// copies (cp.async.bulk, completion counted on an mbarrier) issued
-// kTmaStages tiles ahead by one thread; the block computes from shared memory
-// and stores the results straight to global memory.  One CTA per SM.  Tiles
-// that are not full or not 16-byte aligned are read from global memory
-// directly.  Same arithmetic, so the same bits.
-// ---------------------------------------------------------------------------
-#ifndef OF_TMA_TILE
-#define OF_TMA_TILE 2048
-#endif
-#ifndef OF_TMA_STAGES
-#define OF_TMA_STAGES 4
-#endif
-#ifndef OF_TMA_CTAS
-#define OF_TMA_CTAS 1
-#endif
-constexpr int kTmaTile = OF_TMA_TILE;
-constexpr int kTmaStages = OF_TMA_STAGES;
-static_assert(kTmaTile % (256 * 4) == 0, "a TMA tile is whole float4 rows of the block");
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
-               :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-               " selp.u32 %0, 1, 0, p;\n}"
-               : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-               :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
-}
-
-template <class T, class G, int kSlots>
-struct TmaLayout {
-  static constexpr int kP = kTmaTile * sizeof(T);
-  static constexpr int kG = kTmaTile * sizeof(G);
-  static constexpr int kStage = kP + kG + kSlots * kP;
-};
-
-template <class Op, class T, class G, int CAP>
-__global__ void __launch_bounds__(kThreads, OF_TMA_CTAS)
-mt_step_tma_kernel(const __grid_constant__ MTParams<CAP> mp, const Op op_in,
-                   const float* __restrict__ gscale, uint32_t flags, const StepSrc step) {
-  using GV = typename GradVal<G>::type;
-  using L = TmaLayout<T, G, Op::kSlots>;
-  extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t full[kTmaStages];
-  Op op = op_in;
-  if (step.offset != nullptr) {
-    int64_t t = step.t_base + *step.offset;
-    t = t < 1 ? 1 : (t >= step.rows ? step.rows - 1 : t);
-    op.set_step(step.table[2 * t], step.table[2 * t + 1]);
-  }
-  const bool zero_grad = (flags & OF_FLAG_ZERO_GRAD) != 0;
-  const bool shadow = (flags & OF_FLAG_SHADOW_BF16) != 0;
-  const bool has_scale = gscale != nullptr;
-  const T scale = has_scale ? T(*gscale) : T(1);
-  const int total = mp.tile_end[mp.count - 1];
-  const int ntiles = total > static_cast<int>(blockIdx.x)
-                         ? (total - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1 : 0;
-  if (threadIdx.x == 0) {
-    for (int st = 0; st < kTmaStages; ++st) mbar_init(&full[st], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-
-  struct Where { int ti; int64_t base; int len; };
-  auto locate = [&](int k, int& hint) -> Where {
-    const int tile = static_cast<int>(blockIdx.x) + k * static_cast<int>(gridDim.x);
-    hint = find_tensor(mp, hint, tile);
-    const int tfirst = hint ? mp.tile_end[hint - 1] : 0;
-    const int64_t base = static_cast<int64_t>(tile - tfirst) * kTmaTile;
-    const int64_t rem = mp.n[hint] - base;
-    return Where{hint, base, rem < kTmaTile ? static_cast<int>(rem) : kTmaTile};
-  };
-  auto staged = [&](const Where& w) {
-    if (w.len != kTmaTile) return false;
-    const T* p = static_cast<const T*>(mp.p[w.ti]) + w.base;
-    const G* g = static_cast<const G*>(mp.g[w.ti]) + w.base;
-    if (!aligned(p, 16) || !aligned(g, 16)) return false;
-    if (Op::kSlots >= 1 && !aligned(static_cast<const T*>(mp.s0[w.ti]) + w.base, 16)) return false;
-    if (Op::kSlots >= 2 && !aligned(static_cast<const T*>(mp.s1[w.ti]) + w.base, 16)) return false;
-    if (shadow && !aligned(static_cast<const __nv_bfloat16*>(mp.sh[w.ti]) + w.base, 8)) return false;
-    return true;
-  };
-  int hint_p = 0;
-  auto issue = [&](int k) {                       // thread 0 only
-    const Where w = locate(k, hint_p);
-    uint64_t* bar = &full[k % kTmaStages];
-    unsigned char* st = smem + (k % kTmaStages) * L::kStage;
-    if (!staged(w)) { mbar_arrive(bar); return; }
-    mbar_arrive_expect_tx(bar, L::kStage);
-    bulk_g2s(st, static_cast<const T*>(mp.p[w.ti]) + w.base, L::kP, bar);
-    bulk_g2s(st + L::kP, static_cast<const G*>(mp.g[w.ti]) + w.base, L::kG, bar);
-    if (Op::kSlots >= 1)
-      bulk_g2s(st + L::kP + L::kG, static_cast<const T*>(mp.s0[w.ti]) + w.base, L::kP, bar);
-    if (Op::kSlots >= 2)
-      bulk_g2s(st + 2 * L::kP + L::kG, static_cast<const T*>(mp.s1[w.ti]) + w.base, L::kP, bar);
-  };
-  if (threadIdx.x == 0)
-    for (int k = 0; k < kTmaStages && k < ntiles; ++k) issue(k);
-
-  int hint_c = 0;
-  for (int k = 0; k < ntiles; ++k) {
-    const Where w = locate(k, hint_c);
-    const bool tma = staged(w);
-    uint64_t* bar = &full[k % kTmaStages];
-    unsigned char* st = smem + (k % kTmaStages) * L::kStage;
-    uint32_t tries = 0;
-    while (!mbar_try_wait(bar, (k / kTmaStages) & 1))
-      if (++tries > (1u << 24)) __trap();          // never hang the GPU on a lost transaction
-    T* p = static_cast<T*>(mp.p[w.ti]) + w.base;
-    G* g = static_cast<G*>(mp.g[w.ti]) + w.base;
-    T* s0 = Op::kSlots >= 1 ? static_cast<T*>(mp.s0[w.ti]) + w.base : nullptr;
-    T* s1 = Op::kSlots >= 2 ? static_cast<T*>(mp.s1[w.ti]) + w.base : nullptr;
-    __nv_bfloat16* sh = shadow ? static_cast<__nv_bfloat16*>(mp.sh[w.ti]) + w.base : nullptr;
-    if (tma) {
-      const T* sp = reinterpret_cast<const T*>(st);
-      const G* sg = reinterpret_cast<const G*>(st + L::kP);
-      const T* ss0 = reinterpret_cast<const T*>(st + L::kP + L::kG);
-      const T* ss1 = reinterpret_cast<const T*>(st + 2 * L::kP + L::kG);
-#pragma unroll
-      for (int u = 0; u < kTmaTile / (kThreads * kVec); ++u) {
-        const int j = threadIdx.x + u * kThreads;
-        T vp[4], v0[4], v1[4];
-        GV vg[4];
-        ld4(sp + 4 * j, vp);
-        ld4(sg + 4 * j, vg);
-        if (Op::kSlots >= 1) ld4(ss0 + 4 * j, v0);
-        if (Op::kSlots >= 2) ld4(ss1 + 4 * j, v1);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          T gk = static_cast<T>(vg[e]);
-          if (has_scale) gk = o_mul(gk, scale);
-          op(vp[e], gk, v0[e], v1[e]);
-        }
-        st4(p + 4 * j, vp);
-        if (Op::kSlots >= 1) st4(s0 + 4 * j, v0);
-        if (Op::kSlots >= 2) st4(s1 + 4 * j, v1);
-        if (zero_grad) st4_zero(g + 4 * j);
-        if (shadow) st4_bf16(sh + 4 * j, vp);
-      }
-    } else {
-      for (int e = threadIdx.x; e < w.len; e += kThreads) {
-        T pv = p[e];
-        T a = Op::kSlots >= 1 ? s0[e] : T(0);
-        T b = Op::kSlots >= 2 ? s1[e] : T(0);
-        T gk = static_cast<T>(ld1(g + e));
-        if (has_scale) gk = o_mul(gk, scale);
-        op(pv, gk, a, b);
-        p[e] = pv;
-        if (Op::kSlots >= 1) s0[e] = a;
-        if (Op::kSlots >= 2) s1[e] = b;
-        if (zero_grad) st1_zero(g + e);
-        if (shadow) sh[e] = __float2bfloat16_rn(static_cast<float>(pv));
-      }
-    }
-    __syncthreads();                                // every thread is done with this stage
-    if (threadIdx.x == 0 && k + kTmaStages < ntiles) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic reads before async writes
-      issue(k + kTmaStages);
     }
   }
 }
@@ -808,7 +630,7 @@ int64_t pack(const of_tensor_list* l, int first, int count, MTParams<CAP>& mp, i
 
 template <class Op, class T, class G, int CAP>
 int launch_step_chunk(const of_tensor_list* l, int first, int count, const Op& op,
-                      const float* gscale, uint32_t flags, const StepSrc& step, int max_ctas,
+                      const void* gscale, uint32_t flags, const StepSrc& step, int max_ctas,
                       cudaStream_t s) {
   constexpr int U = Tune<G>::kUnr;
   MTParams<CAP> mp;
@@ -824,31 +646,13 @@ int launch_step_chunk(const of_tensor_list* l, int first, int count, const Op& o
     return check_launch("mt_step_kernel");
   }
   if (tiles > INT32_MAX) return fail(OF_ERR_INVALID, "tensor list too large for one launch");
-  if constexpr (std::is_same<T, float>::value) {
-    if (use_tma() && max_ctas == 0) {
-      using L = TmaLayout<T, G, Op::kSlots>;
-      constexpr int smem = kTmaStages * L::kStage;
-      static bool configured = false;
-      if (!configured) {
-        if (cudaFuncSetAttribute(mt_step_tma_kernel<Op, T, G, CAP>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-          return fail(OF_ERR_CUDA, "cudaFuncSetAttribute(smem %d)", smem);
-        configured = true;
-      }
-      const int64_t ttiles = pack<CAP>(l, first, count, mp, kTmaTile);
-      const int64_t tcap = static_cast<int64_t>(sm_count()) * OF_TMA_CTAS;
-      const int grid = static_cast<int>(ttiles < tcap ? ttiles : tcap);
-      mt_step_tma_kernel<Op, T, G, CAP><<<grid, kThreads, smem, s>>>(mp, op, gscale, flags, step);
-      return check_launch("mt_step_tma_kernel");
-    }
-  }
   const int grid = static_cast<int>(tiles < cap ? tiles : cap);
   mt_step_kernel<Op, T, G, CAP, U><<<grid, kThreads, 0, s>>>(mp, op, gscale, flags, step);
   return check_launch("mt_step_kernel");
 }
 
 template <class Op, class T, class G>
-int launch_step(const of_tensor_list* l, const Op& op, const float* gscale, uint32_t flags,
+int launch_step(const of_tensor_list* l, const Op& op, const void* gscale, uint32_t flags,
                 const StepSrc& step, int max_ctas, cudaStream_t s) {
   int first = 0;
   while (first < l->n) {
@@ -920,7 +724,7 @@ StepSrc step_source(const of_hparams* hp, uint32_t flags) {
 }
 
 template <class T, class G>
-int dispatch_kind(const of_tensor_list* l, const of_hparams* hp, const float* gscale,
+int dispatch_kind(const of_tensor_list* l, const of_hparams* hp, const void* gscale,
                   uint32_t flags, cudaStream_t s) {
   const StepSrc step = step_source(hp, flags);
   flags &= ~OF_FLAG_DEVICE_STEP;
@@ -1141,13 +945,15 @@ const char* of_last_error(void) { return g_err; }
 uint64_t of_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 int of_policy_step_mt(const of_tensor_list* list, const of_hparams* hp,
-                      const float* grad_scale_dev, uint32_t flags, void* stream) {
+                      const void* grad_scale_dev, uint32_t flags, void* stream) {
   g_err[0] = '\0';
   if (!hp) return fail(OF_ERR_INVALID, "hparams is NULL");
   const int slots = slots_of(hp->kind);
   if (slots < 0) return fail(OF_ERR_INVALID, "unknown optimizer kind %d", hp->kind);
-  if (flags & ~(OF_FLAG_ZERO_GRAD | OF_FLAG_SHADOW_BF16 | OF_FLAG_DEVICE_STEP))
+  if (flags & ~(OF_FLAG_ZERO_GRAD | OF_FLAG_SHADOW_BF16 | OF_FLAG_DEVICE_STEP | OF_FLAG_SCALE_F64))
     return fail(OF_ERR_INVALID, "unknown flags 0x%x", flags);
+  if ((flags & OF_FLAG_SCALE_F64) && !grad_scale_dev)
+    return fail(OF_ERR_INVALID, "OF_FLAG_SCALE_F64 without a grad_scale_dev");
   if (!(hp->eta > 0.0)) return fail(OF_ERR_INVALID, "step size must be > 0, got %g", hp->eta);
   if (flags & OF_FLAG_DEVICE_STEP) {
     if (!hp->step_offset_dev || !hp->step_table_dev)
@@ -1168,7 +974,7 @@ int of_policy_step_mt(const of_tensor_list* list, const of_hparams* hp,
 }
 
 int of_sgdm_mt(const of_tensor_list* list, double eta, double alpha, double weight_decay,
-               const float* grad_scale_dev, uint32_t flags, void* stream) {
+               const void* grad_scale_dev, uint32_t flags, void* stream) {
   of_hparams hp;
   memset(&hp, 0, sizeof(hp));
   hp.kind = OF_SGD_MOMENTUM;
@@ -1180,7 +986,7 @@ int of_sgdm_mt(const of_tensor_list* list, double eta, double alpha, double weig
 
 int of_adam_mt(const of_tensor_list* list, double eta, double beta1, double beta2, double epsilon,
                double weight_decay, double bias_correction1, double bias_correction2,
-               int decoupled_weight_decay, const float* grad_scale_dev, uint32_t flags,
+               int decoupled_weight_decay, const void* grad_scale_dev, uint32_t flags,
                void* stream) {
   of_hparams hp;
   memset(&hp, 0, sizeof(hp));
@@ -1363,6 +1169,9 @@ int of_dp_step_multicast(const of_mc_bucket* b, const of_hparams* hp, const floa
   if (b->shard_begin < 0 || b->shard_len < 0 || (b->shard_begin % 4) || (b->shard_len % 4))
     return fail(OF_ERR_INVALID, "shard [%lld, +%lld) must be non-negative multiples of 4",
                 (long long)b->shard_begin, (long long)b->shard_len);
+  if (b->param_dtype != OF_F32 || b->grad_dtype != OF_F32)
+    return fail(OF_ERR_UNSUPPORTED, "multicast step: fp32 parameters and gradients only "
+                "(param dtype %d, grad dtype %d)", b->param_dtype, b->grad_dtype);
   if (!b->mc_grad || !b->mc_param || !b->local_param)
     return fail(OF_ERR_INVALID, "multicast or local buffer is NULL");
   if ((reinterpret_cast<uintptr_t>(b->mc_grad) | reinterpret_cast<uintptr_t>(b->mc_param) |

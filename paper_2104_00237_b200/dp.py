@@ -478,9 +478,20 @@ class DataParallelFusion:
         in the next forward (next bucket prefetched on the comm stream)."""
         from .schedule import StepReport
         self._install()
-        self._install_leaders()
+        record = self._leader_handles is None and self.graph.exec_order is None
+        if record:
+            # leaders must be the first EXECUTED layer of each bucket (module
+            # registration order can differ): record the order in this forward,
+            # which has no deferred bucket to apply yet, and place them after it
+            self._apply_deferred()
+        else:
+            self._install_leaders()
         self.policy.begin_iteration()
-        loss = self.graph.forward(inp)
+        if record:
+            loss = self._forward_recording(inp)
+            self._install_leaders()
+        else:
+            loss = self.graph.forward(inp)
         self._apply_deferred()          # buckets whose leader did not run
         self._mode = "forward-fusion"
         self._backward()
@@ -489,6 +500,25 @@ class DataParallelFusion:
         self._pending_t = self.policy.t
         return StepReport("forward-fusion", loss, None, fused=True,
                           pending_updates=sum(len(b.params) for b in self.buckets if b.pending))
+
+    def _forward_recording(self, inp):
+        """Forward pass that records the layers' first-execution order into
+        ``graph.exec_order`` (temporary pre-hooks on every layer)."""
+        order, seen = [], set()
+
+        def note(i):
+            if i not in seen:
+                seen.add(i)
+                order.append(i)
+        hs = [L.module.register_forward_pre_hook(lambda m, a, i=L.index: note(i))
+              for L in self.graph.layers]
+        try:
+            loss = self.graph.forward(inp)
+        finally:
+            for h in hs:
+                h.remove()
+        self.graph.exec_order = order
+        return loss
 
     def _install_leaders(self) -> None:
         if self._leader_handles is not None:
@@ -542,8 +572,11 @@ class DataParallelFusion:
                 b.pending = False
 
     def flush(self) -> int:
+        """Apply every deferred bucket update now (host-side observation point)."""
         n = sum(len(b.params) for b in self.buckets if b.pending)
         self._apply_deferred()
+        if n:
+            self.graph.flush_gen += 1
         return n
 
     # -- checkpoint / resume ---------------------------------------------------

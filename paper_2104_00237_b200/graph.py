@@ -157,6 +157,10 @@ class Graph:
         self._pre_handles = None
         self._leader_handles = None   # bucketed forward fusion: hooks on bucket leaders only
         self.exec_order = None        # layer indices in first-execution order (recorded)
+        # bumped whenever deferred updates are applied from the host outside an
+        # iteration (flush, checkpoint, state_dict): a CUDA graph captured
+        # before that would apply them again on its next replay
+        self.flush_gen = 0
 
     # -- mixed precision -------------------------------------------------------
 

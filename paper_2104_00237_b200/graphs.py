@@ -17,7 +17,9 @@ as (host index at capture + offset) from a table of the host's own bias
 corrections, so replay j is bit-identical to eager iteration t_capture + j.
 The host policy's ``t`` (and a forward-fusion graph's ``pending_step_t``) is
 advanced per replay so that flushes and checkpoints after replays see the
-right step; stepping the policy eagerly between replays is rejected.
+right step; stepping the policy eagerly between replays is rejected, and so
+is a replay after the host applied the deferred updates (a flush, observe,
+or state_dict between replays): the captured forward would apply them again.
 
 Constraints: inputs are copied into static buffers; a forward-fusion step
 must be captured with ``graph=``: the gradients one replay produces are what
@@ -128,6 +130,7 @@ class CapturedStep:
             self.dstep.offset.fill_(-1)     # replay j runs with offset j
         self.replays = 0
         self._t = policy.t if policy is not None else None
+        self._flush_gen = getattr(graph, "flush_gen", None)
         self._stage = None        # device staging copy of the next call's inputs
         self._staged = False
 
@@ -136,6 +139,12 @@ class CapturedStep:
 
     def __call__(self, inputs=None):
         pol = self.policy
+        if self.owner is not None and getattr(self.owner, "flush_gen", None) != self._flush_gen:
+            # the host applied the deferred (forward-fusion) updates this graph's
+            # next replay would apply again from the same gradients
+            raise StateError("deferred updates were applied on the host (flush / observe / "
+                             "state_dict) after this step was captured; replaying would apply "
+                             "them twice -- capture again to continue")
         if pol is not None:
             if pol.t != self._t:
                 raise StateError("the policy was stepped outside this captured graph; "

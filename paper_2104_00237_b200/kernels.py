@@ -88,8 +88,14 @@ def step_advance(offset: torch.Tensor, delta: int = 1, stream=None) -> None:
 
 
 def policy_step(tl: TensorList, hp: nat.OfHparams, grad_scale, flags: int, stream) -> None:
-    """of_policy_step_mt on ``stream`` (a torch.cuda.Stream or raw handle)."""
-    gs = grad_scale.data_ptr() if grad_scale is not None else None
+    """of_policy_step_mt on ``stream`` (a torch.cuda.Stream or raw handle).
+    ``grad_scale``: None or a 0-dim f32 / f64 device tensor (f64: the flag
+    OF_FLAG_SCALE_F64 is added)."""
+    gs = None
+    if grad_scale is not None:
+        gs = grad_scale.data_ptr()
+        if grad_scale.dtype == torch.float64:
+            flags |= nat.OF_FLAG_SCALE_F64
     st = nat.lib().of_policy_step_mt(tl.ref, ctypes.byref(hp), gs, flags, _handle(stream))
     if st:
         nat.check(st, "of_policy_step_mt")
@@ -130,10 +136,11 @@ class McBucket:
     __slots__ = ("struct", "ref")
 
     def __init__(self, world: int, rank: int, mc_grad_ptr: int, mc_param_ptr: int, local_param,
-                 state0, state1, shard_begin: int, shard_len: int):
+                 state0, state1, shard_begin: int, shard_len: int, dtype=torch.float32):
         def ptr(t):
             return t.data_ptr() if t is not None else None
-        self.struct = nat.OfMcBucket(world, rank, mc_grad_ptr, mc_param_ptr, ptr(local_param),
+        code = dtype_code(dtype)
+        self.struct = nat.OfMcBucket(world, rank, code, code, mc_grad_ptr, mc_param_ptr, ptr(local_param),
                                      ptr(state0), ptr(state1), shard_begin, shard_len)
         self.ref = ctypes.byref(self.struct)
 

@@ -299,21 +299,29 @@ def _check_layout(p, g) -> None:
         if v.dtype != torch.bfloat16 or m.dtype != torch.float32:
             raise ConfigError(f"parameter {p.id}: master weights need a bf16 parameter and an "
                               f"fp32 master, got {v.dtype} / {m.dtype}")
-        if m.shape != v.shape or m.stride() != v.stride() or m.device != v.device:
+        if m.shape != v.shape or not _same_order(m, v) or m.device != v.device:
             raise ConfigError(f"parameter {p.id}: master layout differs from the parameter's")
     elif v.dtype not in (torch.float32, torch.float64):
         raise ConfigError(f"parameter {p.id} has dtype {v.dtype}; expected float32 or float64 "
                           "(or bf16 with master weights)")
-    if not (v.is_contiguous() or v.is_contiguous(memory_format=torch.channels_last)):
+    if not kernels.is_dense(v):
         raise ConfigError(f"parameter {p.id} is not dense; the update kernels need dense storage")
     if g is None:
         return  # checked again once a gradient exists
-    if g.shape != v.shape or g.stride() != v.stride() or g.device != v.device:
+    if g.shape != v.shape or not _same_order(g, v) or g.device != v.device:
         raise ConfigError(f"parameter {p.id}: gradient layout {tuple(g.stride())} on {g.device} "
                           f"differs from parameter layout {tuple(v.stride())} on {v.device}")
     if g.dtype != v.dtype:
         raise ConfigError(f"parameter {p.id}: gradient dtype {g.dtype} with parameter {v.dtype}")
     p._layout_ok = True
+
+
+def _same_order(a, b) -> bool:
+    """Same element order in memory: strides agree on every dimension of size
+    > 1 (a size-1 dimension's stride is arbitrary -- e.g. a 1x1 convolution
+    weight is both contiguous and channels-last) and both are dense."""
+    return (all(sa == sb for n, sa, sb in zip(a.shape, a.stride(), b.stride()) if n > 1)
+            and kernels.is_dense(a) and kernels.is_dense(b))
 
 
 def bytes_per_element_of(kind: str, p) -> int:
@@ -324,15 +332,28 @@ def bytes_per_element_of(kind: str, p) -> int:
     return bytes_per_element(kind, p.value.element_size())
 
 
+def _clip_buffers(graph, dev):
+    """Per-graph clip scalars (sq-norm, f64 factor, f32 coef, workspace),
+    allocated once and rewritten in place by every clip: a captured CUDA graph
+    bakes their addresses into its launches (forward fusion's deferred updates
+    read the factor of the previous replay), so they must never move."""
+    bufs = getattr(graph, "_clip_bufs", None)
+    if bufs is None or bufs[0].device != dev:
+        bufs = (torch.zeros((), dtype=torch.float64, device=dev),
+                torch.ones((), dtype=torch.float64, device=dev),
+                torch.ones((), dtype=torch.float32, device=dev),
+                torch.empty(kernels.sqnorm_workspace_len(), dtype=torch.float64, device=dev))
+        graph._clip_bufs = bufs
+    return bufs
+
+
 def clip_factor(graph, max_norm: float, trace: tr.ScheduleTrace | None = None, stream=None):
     """Device half of the global-norm clip: returns (factor, coef), a 0-dim
-    float64 factor (optim.py:165-168) and its float32 multiplier."""
+    float64 factor (optim.py:165-168) and its float32 rounding, both
+    persistent per-graph buffers rewritten by the next clip."""
     params = graph.parameters
     dev = params[0].value.device
-    sq = torch.empty((), dtype=torch.float64, device=dev)
-    factor = torch.empty((), dtype=torch.float64, device=dev)
-    coef = torch.empty((), dtype=torch.float32, device=dev)
-    ws = torch.empty(kernels.sqnorm_workspace_len(), dtype=torch.float64, device=dev)
+    sq, factor, coef, ws = _clip_buffers(graph, dev)
     by_dtype: dict = {}
     for p in params:
         if trace is not None:
@@ -357,20 +378,29 @@ def clip_factor(graph, max_norm: float, trace: tr.ScheduleTrace | None = None, s
     return factor, coef
 
 
+def grad_scale_for(p, factor, coef):
+    """The scale tensor a parameter's update multiplies its gradient by
+    (optim.py:170 ``p.grad.data *= factor``): numpy scales an f64 gradient by
+    the double factor, an f32 one by the factor rounded to f32."""
+    ref = p.master if p.master is not None else p.value
+    return factor if ref.dtype == torch.float64 else coef
+
+
 def clip_by_global_norm(graph, max_norm: float, trace: tr.ScheduleTrace | None = None,
                         stream=None) -> torch.Tensor:
     """Global-norm clip (optim.py:151-172) as a device reduction.
 
     Returns the clip factor as a 0-dim float64 CUDA tensor (1.0 when nothing
-    is clipped); ``float(result)`` gives the reference's return value (and
-    synchronises).  The factor is attached to every parameter and folded into
-    its next update -- the reference's in-place ``grad *= factor`` without a
-    second pass over the gradients.
+    is clipped; a copy, so it keeps this clip's value); ``float(result)``
+    gives the reference's return value (and synchronises).  The factor is
+    attached to every parameter and folded into its next update -- the
+    reference's in-place ``grad *= factor`` without a second pass over the
+    gradients (in f64 for f64 parameters, f32 otherwise).
     """
     factor, coef = clip_factor(graph, max_norm, trace, stream)
     for p in graph.parameters:
-        p._grad_scale = coef
-    return factor
+        p._grad_scale = grad_scale_for(p, factor, coef)
+    return factor.clone()
 
 
 def newton_step(theta, grad_fn, hessian_fn, eta: float = 1.0):

@@ -35,7 +35,7 @@ from . import checkpoint
 from . import trace as tr
 from .errors import ConfigError, GlobalInfoRequired
 from .graph import Graph, Parameter
-from .optim import OptimizerPolicy, clip_by_global_norm, clip_factor
+from .optim import OptimizerPolicy, clip_by_global_norm, clip_factor, grad_scale_for
 
 BASELINE = "baseline"
 FORWARD_FUSION = "forward-fusion"
@@ -370,7 +370,9 @@ def run_forward_fusion(graph: Graph, policy: OptimizerPolicy, inp, *, timing: bo
         graph.backward()
     scale = None
     if policy.clip_norm is not None:
-        scale = clip_factor(graph, policy.clip_norm, tc)[1]
+        factor, coef = clip_factor(graph, policy.clip_norm, tc)
+        # one scale for the whole engine: the f64 factor for an f64 graph
+        scale = grad_scale_for(graph.parameters[0], factor, coef)
         if tc is not None:
             tc.add_task(tr.CLIP_BARRIER, -1, (tc.tasks[-1].task_id,))
     native.set_all_pending()
@@ -408,6 +410,8 @@ def flush_pending_updates(graph: Graph, policy: OptimizerPolicy,
     else:
         policy.step_params(todo, step_t=graph.pending_step_t)
         n = len(todo)
+    if n:
+        graph.flush_gen += 1
     if trace is not None:
         prev = None
         for p in todo:

@@ -14,7 +14,7 @@ Imports the unmodified reference package (`optfuse`, read-only under
   eta 0.01) for every kind x {chain(3,4), shared-chain(4,4), mul-probe(3)} x
   {f32, f64}, seed 0, under baseline / forward-fusion(+flush) / backward-fusion,
   plus 100-iteration chain(8,32) f32 runs (sgd-momentum with decay, adam eta=1e-4)
-  and clip runs (baseline+clip vs forward-fusion+clip);
+  and clip runs (baseline+clip vs forward-fusion+clip, f32; baseline+clip, f64);
 * traces.json      -- schedule traces (trace.py:102-112 export format) and
   critical-path depths (locality.py:92-100) for chain(n) baseline / BF.
 
@@ -194,6 +194,14 @@ def trajectories() -> None:
                                         sched, inputs, clip=0.05)
             arrays[f"clip|{kind}|{sched}|losses"] = losses
             arrays[f"clip|{kind}|{sched}|params"] = np.concatenate(params)
+    # the same in f64: numpy scales f64 gradients by the double factor itself
+    for kind in ("sgd-momentum", "adam"):
+        g0 = optfuse.build_model("chain", layers=3, width=4, seed=0, precision="f64")
+        inputs = rbench._iteration_inputs(g0, 2, 0, 10)
+        losses, params, _, _ = _run("chain", {"layers": 3, "width": 4}, "f64", 0, kind,
+                                    "baseline", inputs, clip=0.05)
+        arrays[f"clip64|{kind}|baseline|losses"] = losses
+        arrays[f"clip64|{kind}|baseline|params"] = np.concatenate(params)
     np.savez_compressed(OUT / "trajectories.npz", **arrays)
 
 

@@ -295,3 +295,70 @@ def test_sharded_checkpoint_resume_equals_single_process(schedule):
                        start_method="spawn")
     assert out[0] == out[1]
     assert out[0] == _single_process_reference()
+
+
+# -- forward-fusion leaders follow the execution order, not registration ----
+
+class _Reordered(torch.nn.Module):
+    """Three bias-free layers registered c, a, b but executed a -> b -> c: a
+    bucket leader placed by registration order (c) would let a and b read
+    their parameters before the deferred update lands."""
+
+    def __init__(self):
+        super().__init__()
+        gen = torch.Generator().manual_seed(7)
+        self.c = torch.nn.Linear(6, 6, bias=False)
+        self.a = torch.nn.Linear(6, 6, bias=False)
+        self.b = torch.nn.Linear(6, 6, bias=False)
+        with torch.no_grad():
+            for lin in (self.c, self.a, self.b):
+                lin.weight.copy_(torch.rand(6, 6, generator=gen) - 0.5)
+
+    def forward(self, x):
+        return self.c(torch.relu(self.b(torch.relu(self.a(x))))).sum()
+
+
+def _worker_order(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2104_00237_b200 as of
+        from paper_2104_00237_b200.dp import DataParallelFusion
+        g = of.Graph(_Reordered(), None, track_counts=False)
+        pol = of.OptimizerPolicy(KIND, eta=ETA, weight_decay=WD)
+        dp = DataParallelFusion(g, pol, bucket_elems=1 << 20, update_fn=_oracle_update)
+        assert len(dp.buckets) == 1
+        for x in _inputs(rank):
+            dp.run_forward_fusion(x)
+        assert [g.layers[i].name for i in g.exec_order] == ["a", "b", "c"]
+        dp.flush()
+        out[rank] = np.concatenate([p.value.detach().numpy().reshape(-1) for p in g.parameters]).tobytes()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_forward_fusion_leaders_follow_execution_order():
+    from oracle import optim_ref
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().dict()
+    mp.start_processes(_worker_order, args=(2, _free_port(), out), nprocs=2, join=True,
+                       start_method="spawn")
+    assert out[0] == out[1]
+    net = _Reordered()
+    params = list(net.parameters())
+    hp = optim_ref.Hyper(kind=KIND, eta=ETA, weight_decay=WD)
+    slots = [dict() for _ in params]
+    xs = [_inputs(r) for r in range(2)]
+    for it in range(ITERS):
+        grads = []
+        for r in range(2):
+            for p in params:
+                p.grad = None
+            net(xs[r][it]).backward()
+            grads.append([p.grad.numpy().reshape(-1).copy() for p in params])
+        for k, p in enumerate(params):
+            avg = (grads[0][k] + grads[1][k]) * np.float32(0.5)
+            optim_ref.step(KIND, hp, p.detach().numpy().reshape(-1), avg, slots[k], it + 1)
+    want = np.concatenate([p.detach().numpy().reshape(-1) for p in params])
+    assert np.frombuffer(out[0], np.float32).tobytes() == want.tobytes()

@@ -553,6 +553,10 @@ def test_multicast_step_argument_errors():
         kernels.McBucket(1, 0, 0, buf.data_ptr(), buf, st, None, 0, 8),                   # NULL mc
         kernels.McBucket(1, 0, buf.data_ptr() + 4, buf.data_ptr(), buf, st, None, 0, 8),  # align
         kernels.McBucket(1, 0, buf.data_ptr(), buf.data_ptr(), buf, None, None, 0, 8),    # state0
+        kernels.McBucket(1, 0, buf.data_ptr(), buf.data_ptr(), buf, st, None, 0, 8,
+                         dtype=torch.bfloat16),                                            # dtype
+        kernels.McBucket(1, 0, buf.data_ptr(), buf.data_ptr(), buf, st, None, 0, 8,
+                         dtype=torch.float64),                                             # dtype
     ]
     n0 = nat.launch_count()
     for mb in cases:

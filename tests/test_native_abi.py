@@ -30,7 +30,7 @@ def test_library_exports_every_symbol():
     so = nat.lib()
     for name in declared_symbols():
         assert hasattr(so, name), name
-    assert so.of_abi_version() == nat.ABI_VERSION == 2
+    assert so.of_abi_version() == nat.ABI_VERSION == 3
     assert so.of_status_string(0) == b"ok"
     assert so.of_sqnorm_workspace_len() >= 148
 
@@ -62,6 +62,10 @@ def test_invalid_arguments_rejected_before_launch():
     neg = _hp(eta=-1.0)
     assert so.of_policy_step_mt(tl.ref, ctypes.byref(neg), None, 0, None) == nat.OF_ERR_INVALID
     assert so.of_policy_step_mt(tl.ref, ctypes.byref(hp), None, 0x80, None) == nat.OF_ERR_INVALID
+    # ABI 3: an f64 grad scale needs the scale pointer
+    assert so.of_policy_step_mt(tl.ref, ctypes.byref(hp), None, nat.OF_FLAG_SCALE_F64,
+                                None) == nat.OF_ERR_INVALID
+    assert b"SCALE_F64" in so.of_last_error()
     tl.struct.param_dtype = nat.OF_BF16
     tl.grad[0] = 0x3000
     assert so.of_policy_step_mt(tl.ref, ctypes.byref(hp), None, 0, None) == nat.OF_ERR_UNSUPPORTED
@@ -99,6 +103,12 @@ def test_invalid_arguments_rejected_before_launch():
     assert so.of_dp_step_peer(pb.ref, ctypes.byref(sgdm), None, 0, None) == nat.OF_ERR_INVALID
     assert so.of_dp_step_peer(pb.ref, ctypes.byref(sgdm), None, nat.OF_FLAG_ZERO_GRAD,
                               None) == nat.OF_ERR_INVALID
+    # the (experimental) multicast step is fp32 only (ABI 3 dtype fields)
+    mb = kernels.McBucket(1, 0, 0x1000, 0x2000, None, None, None, 0, 8, dtype=torch.bfloat16)
+    mb.struct.local_param = 0x3000
+    mb.struct.state0 = 0x4000
+    assert so.of_dp_step_multicast(mb.ref, ctypes.byref(sgdm), None, 0, None) == nat.OF_ERR_UNSUPPORTED
+    assert b"fp32" in so.of_last_error()
     assert so.of_copy_mt(None, None, None, 3, None) == nat.OF_ERR_INVALID
     nb = (ctypes.c_int64 * 1)(-4)
     one = (ctypes.c_void_p * 1)(0x10)
