@@ -197,6 +197,8 @@ class Engine : public std::enable_shared_from_this<Engine> {
 
   void set_callback(py::object cb) { callback_ = cb.is_none() ? py::object() : cb; }
 
+  void set_debug_skip_ready_wait(bool on) { debug_skip_ready_wait_ = on; }
+
   // -- backward fusion -----------------------------------------------------
   // Arms the hooks for one backward pass.  launch=false only reports
   // gradient readiness to the callback (schedule tracing of the unfused
@@ -537,7 +539,10 @@ class Engine : public std::enable_shared_from_this<Engine> {
     fill_grads(G);
     cudaStream_t cur = current();
     cudaStream_t s = side_ ? side_ : cur;
-    if (side_ && sync) {
+    if (side_ && sync && !debug_skip_ready_wait_) {
+      // the device half of the Appendix B.2 guard: every kernel that reads
+      // the old parameter (this layer's input-gradient computation) was
+      // enqueued on `cur` before this hook fired, so the update waits for them
       cuda_check(cudaEventRecord(G.ready, cur), "cudaEventRecord");
       cuda_check(cudaStreamWaitEvent(side_, G.ready, 0), "cudaStreamWaitEvent");
       s = side_;
@@ -618,6 +623,10 @@ class Engine : public std::enable_shared_from_this<Engine> {
   bool launch_ = true;
   bool hooks_installed_ = false;
   bool profile_ = false;
+  // TEST ONLY (tests/test_race_guard_gpu.py): launch side-stream updates
+  // without waiting for the gradient-ready event -- removes the guard so the
+  // adversarial test can show that it is what keeps the old weights intact
+  bool debug_skip_ready_wait_ = false;
   std::vector<ProfRec> prof_;
   int64_t launches_ = 0;
   py::object callback_, group_cb_;
@@ -669,6 +678,7 @@ PYBIND11_MODULE(_optfuse_engine, m) {
       .def("reset_ff_units", &Engine::reset_ff_units)
       .def("flush", &Engine::flush)
       .def("set_profile", &Engine::set_profile)
+      .def("_debug_skip_ready_wait", &Engine::set_debug_skip_ready_wait)
       .def("take_profile", &Engine::take_profile)
       .def("peek_profile", &Engine::peek_profile)
       .def("launch_group", &Engine::launch_now, py::arg("gi"), py::arg("sync") = true)
