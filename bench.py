@@ -120,6 +120,11 @@ class Dist:
         import torch.distributed as dist
         if self.world > 1 or force:
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            # communicator lines (ranks, transport, NVLS) for the driver's checks, on
+            # stderr so that the result stays the last stdout line
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
             if backend == "nccl":
                 torch.cuda.set_device(self.local)
             dist.init_process_group(backend, rank=self.rank, world_size=self.world)

@@ -43,7 +43,7 @@ extern "C" {
 #endif
 
 /* ABI 3: grad_scale_dev of of_policy_step_mt is untyped (f32, or f64 with
- * OF_FLAG_SCALE_F64); of_mc_bucket carries dtypes. */
+ * OF_FLAG_SCALE_F64); of_mc_bucket carries dtypes; of_wgrad_step. */
 #define OF_ABI_VERSION 3
 
 typedef enum of_status {
@@ -227,6 +227,34 @@ int of_copy_mt(void* const* dst, const void* const* src, const int64_t* nbytes, 
  * bit-identical to the reference's.  dtype: OF_F32 or OF_F64; M <= 65535. */
 int of_exact_matmul(const void* a, const void* b, void* out, int64_t M, int64_t K, int64_t N,
                     int dtype, void* stream);
+
+/* ---- Consumer-fused backward fusion: weight-gradient GEMM + update --------
+ * For a Linear layer y = x W^T (W: [out_features][in_features]) whose
+ * backward has the output gradient dY [tokens][out_features] and the input X
+ * [tokens][in_features] (bf16, row-major, 16-byte aligned), ONE kernel
+ * computes dW = dY^T X on the tensor cores (tcgen05, fp32 accumulator in
+ * TMEM) and applies OptimizerPolicy.step (optim.py:74-148; hp->kind, same
+ * functors as of_policy_step_mt) to the fp32 parameter/master and history
+ * tile by tile from the accumulator: the gradient is never written to memory
+ * (unless grad_dump is given).  With OF_FLAG_SHADOW_BF16 the new parameter is
+ * also written as bf16 to `shadow` (the module's weight).  The caller orders
+ * the layer's input-gradient GEMM (the last reader of the old W) before it on
+ * the same stream (Appendix B.2).  in_features must be a multiple of 32,
+ * out_features of 8.  flags: OF_FLAG_SHADOW_BF16 | OF_FLAG_DEVICE_STEP. */
+typedef struct of_wgrad_args {
+  int64_t out_features;    /* M: rows of W */
+  int64_t in_features;     /* N: columns of W */
+  int64_t tokens;          /* T: rows of dY and X (the reduction) */
+  const void* grad_out_rows; /* dY, bf16 [T][M] */
+  const void* input;       /* X, bf16 [T][N] */
+  void* param;             /* fp32 [M][N]: the parameter, or the master of a bf16 module */
+  void* state0;            /* fp32 [M][N] history slots (optim.py:24-31) */
+  void* state1;
+  void* shadow;            /* bf16 [M][N], with OF_FLAG_SHADOW_BF16 */
+  void* grad_dump;         /* NULL, or fp32 [M][N]: also store dW (parity checks) */
+} of_wgrad_args;
+
+int of_wgrad_step(const of_wgrad_args* args, const of_hparams* hp, uint32_t flags, void* stream);
 
 /* Sum of squares of every grad in `list`, accumulated in f64 with a fixed
  * (deterministic) reduction order (optim.py:160-164).  Uses `workspace_dev`

@@ -32,7 +32,7 @@ KIND_CODES = {"sgd": 0, "sgd-momentum": 1, "adagrad": 2, "rmsprop": 3, "adadelta
 SYMBOLS = ("of_abi_version", "of_status_string", "of_last_error", "of_launch_count",
            "of_policy_step_mt", "of_sgdm_mt", "of_adam_mt", "of_step_advance", "of_dp_step_peer",
            "of_sqnorm_workspace_len", "of_sqnorm_mt", "of_clip_coef", "of_exact_matmul",
-           "of_copy_mt", "of_dp_step_multicast")
+           "of_copy_mt", "of_dp_step_multicast", "of_wgrad_step")
 
 _vp = ctypes.c_void_p
 _PP = ctypes.POINTER(ctypes.c_void_p)
@@ -72,6 +72,13 @@ class OfMcBucket(ctypes.Structure):
                 ("mc_grad", _vp), ("mc_param", _vp), ("local_param", _vp),
                 ("state0", _vp), ("state1", _vp),
                 ("shard_begin", ctypes.c_int64), ("shard_len", ctypes.c_int64)]
+
+
+class OfWgradArgs(ctypes.Structure):
+    _fields_ = [("out_features", ctypes.c_int64), ("in_features", ctypes.c_int64),
+                ("tokens", ctypes.c_int64), ("grad_out_rows", _vp), ("input", _vp),
+                ("param", _vp), ("state0", _vp), ("state1", _vp), ("shadow", _vp),
+                ("grad_dump", _vp)]
 
 
 _lib = None
@@ -117,6 +124,9 @@ def lib():
     so.of_dp_step_multicast.restype = ctypes.c_int
     so.of_dp_step_multicast.argtypes = [ctypes.POINTER(OfMcBucket), ctypes.POINTER(OfHparams), _vp,
                                         ctypes.c_uint32, _vp]
+    so.of_wgrad_step.restype = ctypes.c_int
+    so.of_wgrad_step.argtypes = [ctypes.POINTER(OfWgradArgs), ctypes.POINTER(OfHparams),
+                                 ctypes.c_uint32, _vp]
     so.of_copy_mt.restype = ctypes.c_int
     so.of_copy_mt.argtypes = [_PP, _PP, ctypes.POINTER(ctypes.c_int64), ctypes.c_int, _vp]
     so.of_exact_matmul.restype = ctypes.c_int

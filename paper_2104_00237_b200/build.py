@@ -20,6 +20,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 KERNEL_SRC = PKG / "csrc" / "optfuse_kernels.cu"
+KERNEL_SRCS = [KERNEL_SRC, PKG / "csrc" / "optfuse_wgrad.cu"]
 KERNEL_LIB = PKG / "liboptfuse_b200.so"
 
 
@@ -31,12 +32,12 @@ def _stale(target: Path, sources) -> bool:
 
 
 def build_kernels(force: bool = False, verbose: bool = False) -> Path:
-    deps = [KERNEL_SRC, ROOT / "include" / "optfuse_b200.h"]
+    deps = [*KERNEL_SRCS, PKG / "csrc" / "optfuse_ops.cuh", ROOT / "include" / "optfuse_b200.h"]
     if not force and not _stale(KERNEL_LIB, deps):
         return KERNEL_LIB
     cmd = [NVCC, "-O3", *ARCH, "-lineinfo", "--fmad=false", "-std=c++17",
            "-Xcompiler", "-fPIC", "-shared", "-I", str(ROOT / "include"),
-           "-o", str(KERNEL_LIB), str(KERNEL_SRC)]
+           "-o", str(KERNEL_LIB), *[str(x) for x in KERNEL_SRCS]]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), flush=True)

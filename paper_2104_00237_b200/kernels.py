@@ -154,6 +154,32 @@ def dp_step_multicast(mb: McBucket, hp: nat.OfHparams, grad_scale, flags: int, s
         nat.check(st, "of_dp_step_multicast")
 
 
+def wgrad_step(grad_out, inp, param, state0, state1, hp: nat.OfHparams, *, shadow=None,
+               flags: int = 0, stream=None, grad_dump=None) -> None:
+    """of_wgrad_step: dW = grad_out^T @ inp (bf16 [T, M] and [T, N]) on the tensor
+    cores with the optimizer update applied from the accumulator to the fp32
+    ``param`` [M, N] and its history (and the bf16 ``shadow``); the gradient
+    is not materialised unless ``grad_dump`` (fp32 [M, N]) is given."""
+    T, M = grad_out.shape
+    N = inp.shape[1]
+    if inp.shape[0] != T or tuple(param.shape) != (M, N):
+        raise ConfigError(f"wgrad: shapes {tuple(grad_out.shape)}, {tuple(inp.shape)}, "
+                          f"{tuple(param.shape)} do not form dW = dY^T X")
+    for t, dt in ((grad_out, torch.bfloat16), (inp, torch.bfloat16), (param, torch.float32)):
+        if t.dtype != dt or not t.is_contiguous():
+            raise ConfigError(f"wgrad: expected contiguous {dt}, got {t.dtype}")
+
+    def ptr(t):
+        return t.data_ptr() if t is not None else None
+    if shadow is not None:
+        flags |= nat.OF_FLAG_SHADOW_BF16
+    args = nat.OfWgradArgs(M, N, T, grad_out.data_ptr(), inp.data_ptr(), param.data_ptr(),
+                           ptr(state0), ptr(state1), ptr(shadow), ptr(grad_dump))
+    st = nat.lib().of_wgrad_step(ctypes.byref(args), ctypes.byref(hp), flags, _handle(stream))
+    if st:
+        nat.check(st, "of_wgrad_step")
+
+
 class CopyList:
     """Fixed (dst, src) tensor pairs for ``of_copy_mt`` (pointers captured once)."""
 
