@@ -97,6 +97,8 @@ def parse_args(argv=None):
     ap.add_argument("--extras-out", default="gpurun_out/bench_extras.json",
                     help="where every row, instance and diagnostic goes ('' = nowhere); the "
                          "printed line stays compact")
+    ap.add_argument("--in-situ", type=int, default=1,
+                    help="1: also time the C3 (VGG-16 Adam) backward-fusion launches live (roofline.in_situ_c3_large)")
     ap.add_argument("--headline-only", action="store_true",
                     help="time the headline arm only, nothing else (for profilers)")
     ap.add_argument("--cpu-iters", type=int, default=10, help="CPU baseline: timed iterations")
@@ -273,6 +275,12 @@ WORKLOADS = {
            "desc": ("ResNet-50 on synthetic 3x224x224, batch 64, AdamW (wd 0.05); ours: bf16 model "
                     "with fp32 master weights updated in one pass (bf16 grad in, bf16 param out); "
                     "torch: fp32 params under torch.autocast(bf16)")},
+    "c5m": {"model": "bert_base", "batch": 32, "kind": "adamw", "mixed": True,
+            "hp": {"eta": 1e-4, "weight_decay": 0.01},
+            "torch": ("AdamW", {"lr": 1e-4, "weight_decay": 0.01}),
+            "desc": ("BERT-base pre-training, seq 128, batch 32, AdamW (wd 0.01), bf16 module with "
+                     "fp32 master weights (ours; torch: fp32 params under autocast bf16); adds the "
+                     "consumer-fused rows (Linear weights updated inside their wgrad GEMM)")},
     "c5": {"model": "bert_base", "batch": 32, "kind": "adamw",
            "hp": {"eta": 1e-4, "weight_decay": 0.01},
            "torch": ("AdamW", {"lr": 1e-4, "weight_decay": 0.01}),
@@ -283,7 +291,7 @@ WORKLOADS = {
 
 def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
                 grad_reset=None, opt_impl=None, bucket_elems=None, graphed=None,
-                workload="c2", channels_last=None):
+                workload="c2", channels_last=None, consumer=False):
     """Returns (step_fn, graph_or_model, policy_or_opt).  ``opt_impl`` selects
     the unfused torch.optim baseline ("foreach" | "fused") or "none" (forward
     + backward only, no update: the lower bound any fusion can reach);
@@ -395,11 +403,15 @@ def make_runner(args, batch: int, schedule: str, device, seed=0, workers=None,
                                              prefetch=pre).loss
         else:
             be = args.bucket_elems if bucket_elems is None else bucket_elems
+            cf = None
+            if consumer:   # Linear weights updated inside their wgrad GEMM (tcgen05)
+                from paper_2104_00237_b200.consumer import ConsumerFusion
+                cf = ConsumerFusion(g, pol)
 
             def run(inp):
                 return of.run_backward_fusion(g, pol, inp, workers=w, timing=False,
                                               bucket_elems=be, update_ctas=ctas,
-                                              update_priority=prio).loss
+                                              update_priority=prio, consumer=cf).loss
         owner = g
     if graphed:
         ours = isinstance(pol, of.OptimizerPolicy)
@@ -600,6 +612,51 @@ def measure_in_graph(args, device, peaks, flush, reps: int = 20) -> dict:
             "replays": reps, "step_us_min_max": [round(min(ms) * 1e3, 3), round(max(ms) * 1e3, 3)]}
 
 
+def measure_live_launches(args, wl: str, device, peaks, iters: int = 3) -> dict:
+    """In-situ roofline of one config's backward-fusion launches (per layer,
+    side stream, eager): a CUDA event pair around every update launch while it
+    runs beside the backward (engine profile mode), algorithmic bytes of each
+    launch / its duration.  Reported over all launches and over the large
+    ones (>= 64 MB: the update-bound layers, e.g. VGG-16's fc6 at 2.9 GB)."""
+    import torch
+
+    from paper_2104_00237_b200.optim import bytes_per_element_of
+    world, dp, args.world, args.dp = getattr(args, "world", 1), getattr(args, "dp", False), 1, False
+    try:
+        step, g, pol = make_runner(args, WORKLOADS[wl]["batch"], "backward-fusion", device, workers=2,
+                                   bucket_elems=0, graphed=False, workload=wl,
+                                   channels_last=wl in ("c4",))
+    finally:
+        args.world, args.dp = world, dp
+    for _ in range(3):
+        step()
+    eng = next(e for k, e in g._engines.items() if k[1])
+    eng.native.take_profile()
+    eng.native.set_profile(True)
+    for _ in range(iters):
+        step()
+    eng.native.set_profile(False)
+    torch.cuda.synchronize()
+    rec = eng.native.take_profile()
+    bpe = bytes_per_element_of(pol.kind, g.parameters[0])
+
+    def summ(rows):
+        if not rows:
+            return None
+        b = sum(n for _, n in rows) * bpe
+        t = sum(ms for ms, _ in rows) / 1e3
+        return {"launches": len(rows) // iters, "bytes_per_step": b // iters,
+                "achieved_gbs": round(b / t / 1e9, 1), "frac": round(b / t / 1e9 / peaks["hbm_gbs"], 4)}
+    big = max(rec, key=lambda r: r[1])
+    out = {"all": summ(rec), "large": summ([r for r in rec if r[1] * bpe >= 64 << 20]),
+           "largest_launch": {"bytes": big[1] * bpe, "us": round(big[0] * 1e3, 2),
+                              "frac": round(big[1] * bpe / (big[0] / 1e3) / 1e9 / peaks["hbm_gbs"], 4)},
+           "method": "event pair around each launch, side stream beside the eager backward"}
+    del step, g, pol
+    torch.cuda.empty_cache()
+    return out
+
+
 def cpu_baseline(args) -> dict:
     """The reference arm's measurement (same function, same workload) on a
     bounded sample: W warm-up + K timed iterations on all host cores."""
@@ -694,10 +751,16 @@ def headline_arms(args) -> list:
     arms += [("torch.optim.SGD(foreach)", {"schedule": "baseline", "opt_impl": "foreach"}),
              ("torch.optim.SGD(fused)", {"schedule": "baseline", "opt_impl": "fused"}),
              (FLOOR, {"schedule": "baseline", "opt_impl": "none"})]
+    if getattr(args, "dp", False) or getattr(args, "force_dp", False):
+        # data parallel: the torch arms run under DDP, so the no-update arm is DDP's
+        # forward + backward + gradient all-reduce -- a floor for the DDP arms only
+        arms = [(FLOOR_DDP if n == FLOOR else "DDP+" + n if n.startswith("torch") else n, kw)
+                for n, kw in arms]
     return arms
 
 
 FLOOR = "fwd+bwd only (no update: lower bound)"
+FLOOR_DDP = "DDP fwd+bwd+all-reduce only (no update; floor of the DDP arms)"
 
 
 def run_ours(args) -> dict:
@@ -778,6 +841,7 @@ def run_ours(args) -> dict:
         return round(med[name], 4) if name in med else None
 
     unfused_torch = "DDP + " if args.dp else ""
+    tp = "DDP+" if args.dp else ""
     res = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": dist.world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -787,12 +851,12 @@ def run_ours(args) -> dict:
                       "parallelism": f"dp{dist.world}", "instances": args.instances,
                       "l2": "256 MiB flush before every timed step, outside its events"},
            "unfused": {"ours_baseline_ms": med_ms("ours:baseline"),
-                       "torch_foreach_ms": med_ms("torch.optim.SGD(foreach)"),
-                       "torch_fused_ms": med_ms("torch.optim.SGD(fused)"),
-                       "fwd_bwd_floor_ms": med_ms(FLOOR),
+                       "torch_foreach_ms": med_ms(tp + "torch.optim.SGD(foreach)"),
+                       "torch_fused_ms": med_ms(tp + "torch.optim.SGD(fused)"),
+                       ("ddp_fwd_bwd_ms" if tp else "fwd_bwd_floor_ms"): med_ms(FLOOR_DDP if tp else FLOOR),
                        "speedup_vs_ours_unfused": ratio("ours:baseline"),
-                       "speedup_vs_torch_foreach": ratio("torch.optim.SGD(foreach)"),
-                       "speedup_vs_torch_fused": ratio("torch.optim.SGD(fused)"),
+                       "speedup_vs_torch_foreach": ratio(tp + "torch.optim.SGD(foreach)"),
+                       "speedup_vs_torch_fused": ratio(tp + "torch.optim.SGD(fused)"),
                        "torch_arm": unfused_torch + "torch.optim, same mode"},
            "gpu_launches": int(launches)}
     extras = {"rows": {k: {"ms_per_step": round(med[k], 4),
@@ -827,6 +891,11 @@ def run_ours(args) -> dict:
                        "bytes_per_launch": round(prim["avg_bytes"]),
                        "us_per_launch": round(prim["avg_us"], 3),
                        "launches_per_step": prim["launches_per_step"]}
+    if args.in_situ:
+        # the update-bound config's large layers (VGG-16 Adam), live beside its backward
+        c3 = measure_live_launches(args, "c3", device, peaks)
+        res["roofline"]["in_situ_c3_large"] = {k: c3["large"][k] for k in ("achieved_gbs", "frac")}
+        extras["in_situ_c3"] = c3
     extras["roofline"] = {
         "method": ("CUDA events captured as event-record nodes around each update launch of the "
                    "headline graph, read after every replay (live, beside the backward)")
@@ -910,6 +979,11 @@ def _variants_extra(wl: str):
               (pre + "ours:backward-fusion(w=1,per-layer)", "backward-fusion", 1, None, 0, gph)]
         if WORKLOADS[wl].get("mixed"):
             v.append((pre + OWN_LB, "baseline", None, "none-mixed", 0, gph))
+        if wl == "c5m":
+            v.append((pre + "ours:backward-fusion(w=2,per-layer)+consumer", "backward-fusion+consumer",
+                      2, None, 0, gph))
+            v.append((pre + "ours:backward-fusion(w=1,per-layer)+consumer", "backward-fusion+consumer",
+                      1, None, 0, gph))
     return v
 
 
@@ -929,8 +1003,10 @@ def run_extra(args, wl: str, device, dist, flush) -> dict:
             if name in failed:
                 continue
             try:
-                st, *_ = make_runner(args, b, sch, device, workers=w, opt_impl=opt, bucket_elems=be,
-                                     graphed=gph, workload=wl, channels_last=wl in ("c4",))
+                cons = sch.endswith("+consumer")
+                st, *_ = make_runner(args, b, sch.replace("+consumer", ""), device, workers=w,
+                                     opt_impl=opt, bucket_elems=be, graphed=gph, workload=wl,
+                                     channels_last=wl in ("c4",), consumer=cons)
                 times[name].append(timed(st, steps, warm, dist, flush))
             except Exception as e:  # noqa: BLE001 -- report, keep the other rows
                 failed[name] = f"{type(e).__name__}: {str(e).splitlines()[0][:160] if str(e) else ''}"

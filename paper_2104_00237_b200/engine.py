@@ -33,7 +33,7 @@ def native_engine_module():
     return _mod
 
 
-def launch_groups(graph, bucket_elems: int = 0) -> list:
+def launch_groups(graph, bucket_elems: int = 0, exclude=frozenset()) -> list:
     """Backward-fusion launch groups as lists of parameter ids.
 
     Each parameter belongs to the first layer (registration order) binding it,
@@ -42,7 +42,7 @@ def launch_groups(graph, bucket_elems: int = 0) -> list:
     order (last layer first), until a bucket holds at least that many
     elements -- fewer, larger launches for networks of many small layers.
     """
-    groups, seen = [], set()
+    groups, seen = [], set(exclude)   # excluded: updated by their consumer kernel
     for layer in graph.layers:
         ids = [p.id for p in layer.params if p.id not in seen]
         seen.update(ids)
@@ -65,13 +65,13 @@ def launch_groups(graph, bucket_elems: int = 0) -> list:
 
 class FusionEngine:
     def __init__(self, graph, policy, side_stream: bool, bucket_elems: int = 0,
-                 priority: str = "high"):
+                 priority: str = "high", exclude=frozenset()):
         m = native_engine_module()
         self.graph = graph
         self.kind = policy.kind
         self.side = side_stream
         self.bucket_elems = bucket_elems
-        self.groups = launch_groups(graph, bucket_elems)
+        self.groups = launch_groups(graph, bucket_elems, exclude)
         # CUDA stream priorities: lower number = higher priority (-1 is the
         # highest torch exposes, 0 the default)
         self.stream = (torch.cuda.Stream(priority=-1 if priority == "high" else 0)

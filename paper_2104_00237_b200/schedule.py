@@ -165,12 +165,13 @@ class _TraceRecorder:
 
 
 def _engine(graph: Graph, policy: OptimizerPolicy, side: bool, bucket_elems: int = 0,
-            priority: str = "high"):
+            priority: str = "high", exclude=frozenset()):
     from .engine import FusionEngine
-    key = (policy.kind, side, bucket_elems) + (() if priority == "high" else (priority,))
+    key = ((policy.kind, side, bucket_elems) + (() if priority == "high" else (priority,))
+           + ((("consumer", exclude),) if exclude else ()))
     eng = graph._engines.get(key)
     if eng is None:
-        eng = FusionEngine(graph, policy, side, bucket_elems, priority)
+        eng = FusionEngine(graph, policy, side, bucket_elems, priority, exclude)
         graph._engines[key] = eng
     return eng
 
@@ -433,7 +434,7 @@ def default_update_ctas() -> int:
 def run_backward_fusion(graph: Graph, policy: OptimizerPolicy, inp, workers: int = 1, *,
                         timing: bool = True, trace: bool = False,
                         bucket_elems: int = 0, update_ctas: int | None = None,
-                        update_priority: str = "high") -> StepReport:
+                        update_priority: str = "high", consumer=None) -> StepReport:
     """Eager schedule: update each layer as soon as its gradients are complete.
 
     ``workers=1`` issues each update inline on the autograd stream;
@@ -446,6 +447,9 @@ def run_backward_fusion(graph: Graph, policy: OptimizerPolicy, inp, workers: int
     "low") is the side stream's priority: high mirrors the reference runner's
     step-first heap; low lets a GPU-bound backward keep the SMs and the
     updates fill the gaps.
+    ``consumer`` (a consumer.ConsumerFusion of this graph and policy): its
+    Linear weights are updated inside their weight-gradient GEMM (no gradient
+    in memory, no separate launch); every other parameter as above.
     Raises GlobalInfoRequired, mutating nothing, for policies or transforms
     that must see all gradients first (schedule.py:174-177).
     """
@@ -461,9 +465,14 @@ def run_backward_fusion(graph: Graph, policy: OptimizerPolicy, inp, workers: int
         raise ConfigError(f"bucket_elems must be >= 0, got {bucket_elems}")
     if update_priority not in ("high", "low"):
         raise ConfigError(f"update_priority must be 'high' or 'low', got {update_priority!r}")
+    if consumer is not None and (consumer.graph is not graph or consumer.policy is not policy):
+        raise ConfigError("consumer fusion was built for another graph or policy")
+    if consumer is not None and trace:
+        raise ConfigError("schedule traces do not cover consumer-fused layers")
     _leave_forward_fusion(graph, policy)
     eng = _engine(graph, policy, workers > 1, bucket_elems,
-                  update_priority if workers > 1 else "high")
+                  update_priority if workers > 1 else "high",
+                  consumer.id_set if consumer is not None else frozenset())
     policy.begin_iteration()
     if workers > 1 and update_ctas is None:
         update_ctas = default_update_ctas()
@@ -480,10 +489,14 @@ def run_backward_fusion(graph: Graph, policy: OptimizerPolicy, inp, workers: int
         rec = _TraceRecorder(graph, tc, eng.groups)
         native.set_callback(rec)
     native.bf_begin(True)
+    if consumer is not None:
+        consumer.active = True
     try:
         graph.backward(tc)
     finally:
         native.disarm()
+        if consumer is not None:
+            consumer.active = False
         if rec is not None:
             native.set_callback(None)
     native.bf_finish()
