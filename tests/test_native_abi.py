@@ -131,3 +131,25 @@ def test_check_raises_native_error():
     so.of_policy_step_mt(None, None, None, 0, None)
     with pytest.raises(NativeLibraryError, match="invalid"):
         nat.check(nat.OF_ERR_INVALID, "of_policy_step_mt")
+
+
+def test_no_host_function_compiled_to_an_exit_stub():
+    """nvcc compiles a host function template that calls a __device__-only
+    helper into `exit(1)` without an error; such a launcher would kill the
+    process silently on its first call.  Every host function of the library's
+    own code must therefore be free of calls to exit()."""
+    import shutil
+    import subprocess
+    if shutil.which("objdump") is None:
+        pytest.skip("objdump not installed")
+    out = subprocess.run(["objdump", "-d", "--no-show-raw-insn", "-C", str(nat.LIB_PATH)],
+                         capture_output=True, text=True, check=True).stdout
+    stubs, fn = [], None
+    for line in out.splitlines():
+        m = re.match(r"^[0-9a-f]+ <(.*)>:$", line)
+        if m:
+            fn = m.group(1)
+        elif fn and "exit@plt" in line and ("ofk::" in fn or "anonymous namespace" in fn
+                                             or fn.startswith("of_")):
+            stubs.append(fn)
+    assert not stubs, stubs[:5]

@@ -1,6 +1,7 @@
-"""Backward fusion on a GPU-bound step (diagnostic): BERT-base b32 AdamW,
-graphed; side-stream update grid capped at various CTA counts and both
-stream priorities, against the baseline schedule and the floor."""
+"""Backward fusion on a GPU-bound step (diagnostic): one config (c3 | c4 | c5),
+graphed, true fp32 (TF32 off, as bench.py); side-stream update grid capped at
+various CTA counts, both stream priorities, per-layer and 1M buckets, against
+the baseline schedule.  Arms are interleaved, --instances rounds, medians."""
 
 import json
 import sys
@@ -20,38 +21,47 @@ def main():
     wl = sys.argv[1] if len(sys.argv) > 1 else "c5"
     torch.backends.cudnn.benchmark = True
     torch.backends.cudnn.benchmark_limit = 0
-    torch.backends.cuda.matmul.allow_tf32 = True
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.allow_tf32 = False
     dev = torch.device("cuda", 0)
     args = bench.parse_args([])
     args.world, args.dp = 1, False
     dist = bench.Dist()
     buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     W = bench.WORKLOADS[wl]
-    out = {}
-    for name, sched, kw in (("baseline", "baseline", {}),
-                            ("bf_1M", "backward-fusion", dict(workers=2, bucket_elems=1 << 20)),
-                            ("bf_1M_cap37", "backward-fusion", dict(workers=2, bucket_elems=1 << 20, update_ctas=37)),
-                            ("bf_1M_cap74", "backward-fusion", dict(workers=2, bucket_elems=1 << 20, update_ctas=74)),
-                            ("bf_1M_cap148", "backward-fusion", dict(workers=2, bucket_elems=1 << 20, update_ctas=148)),
-                            ("bf_1M_cap296", "backward-fusion", dict(workers=2, bucket_elems=1 << 20, update_ctas=296)),
-                            ("bf_1M_low", "backward-fusion", dict(workers=2, bucket_elems=1 << 20, update_priority="low")),
-                            ("bf_1M_cap74_low", "backward-fusion", dict(workers=2, bucket_elems=1 << 20, update_ctas=74, update_priority="low")),
-                            ("bf_4M_cap148", "backward-fusion", dict(workers=2, bucket_elems=1 << 22, update_ctas=148))):
-        g = of.build_classifier(W["model"], device=dev, channels_last=wl in ("c4",))
-        g.track_counts = False
-        x, y = synthetic_batch(W["model"], W["batch"], device=dev)
-        if W.get("mixed"):
-            g.use_master_weights()
-            x = x.to(torch.bfloat16)
-        pol = of.OptimizerPolicy(W["kind"], **W["hp"], grad_reset="none")
-        if sched == "baseline":
-            run = lambda inp: of.run_baseline(g, pol, inp, timing=False).loss  # noqa: E731
-        else:
-            run = lambda inp, kw=kw: of.run_backward_fusion(g, pol, inp, timing=False, **kw).loss  # noqa: E731
-        cap = CapturedStep(run, (x, y), policy=pol, graph=g)
-        out[name] = round(bench.timed(cap, 10, 3, dist, buf.zero_), 3)
-        del cap, g
-        torch.cuda.empty_cache()
+    arms = [("baseline", "baseline", {})]
+    for bucket, tag in ((1 << 20, "1M"), (0, "layer")):
+        for cap in (0, 8, 16, 32, 74):
+            for prio in ("high", "low"):
+                if prio == "low" and cap not in (0, 16):
+                    continue
+                kw = dict(workers=2, bucket_elems=bucket, update_ctas=cap, update_priority=prio)
+                arms.append((f"bf_{tag}_cap{cap}_{prio}", "backward-fusion", kw))
+    arms.append(("bf_layer_inline", "backward-fusion", dict(workers=1, bucket_elems=0)))
+    instances = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+    res = {name: [] for name, _, _ in arms}
+    for _ in range(instances):
+        for name, sched, kw in arms:
+            g = of.build_classifier(W["model"], device=dev, channels_last=wl in ("c4",))
+            g.track_counts = False
+            x, y = synthetic_batch(W["model"], W["batch"], device=dev)
+            if W.get("mixed"):
+                g.use_master_weights()
+                x = x.to(torch.bfloat16)
+            pol = of.OptimizerPolicy(W["kind"], **W["hp"], grad_reset="none")
+            if sched == "baseline":
+                run = lambda inp: of.run_baseline(g, pol, inp, timing=False).loss  # noqa: E731
+            else:
+                run = lambda inp, kw=kw: of.run_backward_fusion(g, pol, inp, timing=False, **kw).loss  # noqa: E731
+            cap = CapturedStep(run, (x, y), policy=pol, graph=g)
+            res[name].append(round(bench.timed(cap, 10, 3, dist, buf.zero_), 3))
+            del cap, g
+            torch.cuda.empty_cache()
+    import statistics
+    out = {name: {"median_ms": statistics.median(v), "instances_ms": v} for name, v in res.items()}
+    base = out["baseline"]["median_ms"]
+    for v in out.values():
+        v["vs_baseline"] = round(base / v["median_ms"], 4)
     print(json.dumps({wl: out}))
 
 

@@ -63,8 +63,9 @@ def main():
     for u in upd:
         dur = u["end"] - u["start"]
         # union of other-stream kernel intervals intersected with [start, end)
+        # (kernels of one stream never overlap, so any overlap is another stream's)
         iv = sorted((max(o["start"], u["start"]), min(o["end"], u["end"])) for o in other
-                    if o["stream"] != u["stream"] and o["end"] > u["start"] and o["start"] < u["end"])
+                    if o["end"] > u["start"] and o["start"] < u["end"])
         covered, cur = 0.0, None
         for a, b in iv:
             if cur is None or a > cur[1]:
