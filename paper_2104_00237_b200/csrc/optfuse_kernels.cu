@@ -86,9 +86,6 @@ constexpr int kVec = 4;
 #ifndef OF_CS
 #define OF_CS 0
 #endif
-#ifndef OF_SMALL_SLOTS   // 1-vector build up to this many slots per resident thread
-#define OF_SMALL_SLOTS 1
-#endif
 constexpr int kUnroll = OF_UNROLL;
 constexpr int kTile = kThreads * kVec * kUnroll;  // elements per tile
 constexpr int kCtasPerSm = 8;
@@ -220,13 +217,12 @@ __host__ __device__ __forceinline__ bool aligned(const void* p, unsigned a) {
   return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0;
 }
 
-// Per gradient type: vectors per thread per round and the CTAs per SM the
-// register budget must allow.  fp32/f64 gradients: 4 vectors of every stream
-// in flight per thread at 2 CTAs/SM (measured best for VGG-16 / BERT); bf16
-// gradients (fp32 master + bf16 shadow, 8 streams per element): 2 vectors at
-// 4 CTAs/SM -- the 4-vector build needs 108 registers and stalls at 16
-// warps/SM (ncu: 52% of DRAM peak on ResNet-50), the 2-vector one reaches
-// 0.80 of the copy peak.
+// Per gradient type: vectors per thread per tile and the CTAs per SM the
+// register budget must allow.  fp32/f64 gradients: 4 vectors in flight per
+// thread at 2 CTAs/SM (measured best for VGG-16 / BERT); bf16 gradients (fp32
+// master + bf16 shadow, 8 streams per element): 2 vectors at 4 CTAs/SM -- the
+// 4-vector build needs 108 registers and stalls at 16 warps/SM (ncu: 52% of
+// DRAM peak on ResNet-50), the 2-vector one reaches 0.80 of the copy peak.
 template <class G> struct Tune {
   static constexpr int kUnr = OF_UNROLL;
   static constexpr int kMinBlocks = OF_MIN_BLOCKS;
@@ -236,142 +232,92 @@ template <> struct Tune<__nv_bfloat16> {
   static constexpr int kMinBlocks = OF_MIN_BLOCKS_BF16;
 };
 
-// Parameter block of one update launch.  The tensors are laid end to end in a
-// virtual space of 4-element "vector slots" (tensor i owns ceil(n_i / 4) of
-// them, ending at vend[i]); every CTA owns one equal, contiguous share of that
-// space, whatever the tensor boundaries.  A parameter set of many small
-// tensors (MobileNetV2: 150 of 158 under 64 K elements) therefore loads every
-// SM equally in a single wave, instead of one CTA per tensor-aligned tile
-// with most CTAs on a few-hundred-element tail.
-template <int CAP>
-struct StepParams {
-  void* p[CAP];
-  void* g[CAP];
-  void* s0[CAP];
-  void* s1[CAP];
-  void* sh[CAP];
-  int64_t n[CAP];
-  int32_t vend[CAP];    // inclusive prefix sum of vector slots
-  uint8_t vok[CAP];     // 1: every stream of tensor i is aligned for vector access
-  int32_t count;
-  int32_t per_cta;      // vector slots per CTA
-};
-
-// First tensor whose slots end after slot j, searching [lo, count).
-__device__ __forceinline__ int slot_owner(const int32_t* vend, int lo, int count, int32_t j) {
-  int hi = count - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (j < vend[mid]) hi = mid; else lo = mid + 1;
-  }
-  return lo;
-}
-
-// One multi-tensor policy step over this CTA's share of the slot space.  Each
-// thread takes slots j = share start + tid + k * kThreads: a warp covers 32
-// consecutive slots (512 contiguous bytes of every fp32 stream), and all the
-// loads of UNR slots are issued before any math.  A slot at the end of a
-// tensor (n % 4 != 0) or of an unaligned tensor goes element by element; the
-// arithmetic is the same functor either way, so the result does not depend on
-// where a tensor lands in the slot space.
+// One multi-tensor policy step.  T: param/state type; G: grad type; UNR:
+// vectors per thread per tile (tile = 256 * 4 * UNR elements).  Small lists
+// use UNR=1 so that even a few MB spread over more CTAs than there are SMs.
 template <class Op, class T, class G, int CAP, int UNR>
 __global__ void __launch_bounds__(kThreads, Tune<G>::kMinBlocks)
-mt_step_kernel(const __grid_constant__ StepParams<CAP> mp, const Op op_in,
+mt_step_kernel(const __grid_constant__ MTParams<CAP> mp, const Op op_in,
                const void* __restrict__ gscale, uint32_t flags, const StepSrc step) {
   using GV = typename GradVal<G>::type;
-  __shared__ int32_t s_vend[CAP];
-  for (int i = threadIdx.x; i < mp.count; i += kThreads) s_vend[i] = mp.vend[i];
   Op op = op_in;
   if (step.offset != nullptr) {  // OF_FLAG_DEVICE_STEP: this replay's step index
     int64_t t = step.t_base + *step.offset;
     t = t < 1 ? 1 : (t >= step.rows ? step.rows - 1 : t);
     op.set_step(step.table[2 * t], step.table[2 * t + 1]);
   }
+  constexpr int kTileU = kThreads * kVec * UNR;
   constexpr int kRoundMax = sizeof(T) == 8 ? 2 : 4;
   constexpr int kRound = UNR < kRoundMax ? UNR : kRoundMax;  // vectors in flight per thread
-  const int count = mp.count;
-  const int32_t total = mp.vend[count - 1];
-  const int64_t beg64 = static_cast<int64_t>(blockIdx.x) * mp.per_cta;
-  const int32_t beg = static_cast<int32_t>(beg64 < total ? beg64 : total);
-  const int32_t end = static_cast<int32_t>(beg64 + mp.per_cta < total ? beg64 + mp.per_cta : total);
+  const int total = mp.tile_end[mp.count - 1];
   const bool zero_grad = (flags & OF_FLAG_ZERO_GRAD) != 0;
   const bool shadow = (flags & OF_FLAG_SHADOW_BF16) != 0;
   const bool has_scale = gscale != nullptr;
   const T scale = load_scale<T>(gscale, flags);
-  __syncthreads();
   int ti = 0;
-  for (int32_t base = beg + threadIdx.x; base < end; base += kThreads * kRound) {
-    T vp[kRound][4], v0[kRound][4], v1[kRound][4];
-    GV vg[kRound][4];
-    int own[kRound];
-    int64_t off[kRound];
-    int len[kRound];
+  for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+    ti = find_tensor(mp, ti, tile);
+    const int tfirst = ti ? mp.tile_end[ti - 1] : 0;
+    const int64_t base = static_cast<int64_t>(tile - tfirst) * kTileU;
+    const int64_t rem = mp.n[ti] - base;
+    const int len = rem < kTileU ? static_cast<int>(rem) : kTileU;
+    T* p = static_cast<T*>(mp.p[ti]) + base;
+    G* g = static_cast<G*>(mp.g[ti]) + base;
+    T* s0 = Op::kSlots >= 1 ? static_cast<T*>(mp.s0[ti]) + base : nullptr;
+    T* s1 = Op::kSlots >= 2 ? static_cast<T*>(mp.s1[ti]) + base : nullptr;
+    __nv_bfloat16* sh = shadow ? static_cast<__nv_bfloat16*>(mp.sh[ti]) + base : nullptr;
+    const bool vec_ok = aligned(p, 16) && aligned(g, 4 * sizeof(G)) &&
+                        (Op::kSlots < 1 || aligned(s0, 16)) && (Op::kSlots < 2 || aligned(s1, 16)) &&
+                        (!shadow || aligned(sh, 8));
+    int scalar_from = 0;
+    if (vec_ok) {
+      const int nvec = len / kVec;
 #pragma unroll
-    for (int u = 0; u < kRound; ++u) {
-      const int32_t j = base + u * kThreads;
-      len[u] = 0;
-      if (j < end) {
-        ti = slot_owner(s_vend, ti, count, j);
-        const int32_t first = ti ? s_vend[ti - 1] : 0;
-        const int64_t e = static_cast<int64_t>(j - first) * kVec;
-        const int64_t rem = mp.n[ti] - e;
-        own[u] = ti;
-        off[u] = e;
-        len[u] = rem < kVec ? static_cast<int>(rem) : kVec;
-        const T* p = static_cast<const T*>(mp.p[ti]) + e;
-        const G* g = static_cast<const G*>(mp.g[ti]) + e;
-        const T* a = Op::kSlots >= 1 ? static_cast<const T*>(mp.s0[ti]) + e : nullptr;
-        const T* b = Op::kSlots >= 2 ? static_cast<const T*>(mp.s1[ti]) + e : nullptr;
-        if (len[u] == kVec && mp.vok[ti]) {
-          ld4(p, vp[u]);
-          ld4s(g, vg[u]);
-          if (Op::kSlots >= 1) ld4s(a, v0[u]);
-          if (Op::kSlots >= 2) ld4s(b, v1[u]);
-        } else {
+      for (int r = 0; r < UNR; r += kRound) {
+        T vp[kRound][4], v0[kRound][4], v1[kRound][4];
+        GV vg[kRound][4];
 #pragma unroll
-          for (int k = 0; k < kVec; ++k) {
-            const bool in = k < len[u];
-            vp[u][k] = in ? p[k] : T(0);
-            vg[u][k] = in ? static_cast<GV>(ld1(g + k)) : GV(0);
-            v0[u][k] = (Op::kSlots >= 1 && in) ? a[k] : T(0);
-            v1[u][k] = (Op::kSlots >= 2 && in) ? b[k] : T(0);
+        for (int u = 0; u < kRound; ++u) {
+          const int j = threadIdx.x + (r + u) * kThreads;
+          if (j < nvec) {
+            ld4(p + 4 * j, vp[u]);
+            ld4s(g + 4 * j, vg[u]);
+            if (Op::kSlots >= 1) ld4s(s0 + 4 * j, v0[u]);
+            if (Op::kSlots >= 2) ld4s(s1 + 4 * j, v1[u]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kRound; ++u) {
+          const int j = threadIdx.x + (r + u) * kThreads;
+          if (j < nvec) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              T gk = static_cast<T>(vg[u][k]);
+              if (has_scale) gk = o_mul(gk, scale);  // grad *= clip factor (optim.py:170)
+              op(vp[u][k], gk, v0[u][k], v1[u][k]);
+            }
+            st4(p + 4 * j, vp[u]);
+            if (Op::kSlots >= 1) st4s(s0 + 4 * j, v0[u]);
+            if (Op::kSlots >= 2) st4s(s1 + 4 * j, v1[u]);
+            if (zero_grad) st4_zero(g + 4 * j);
+            if (shadow) st4_bf16(sh + 4 * j, vp[u]);
           }
         }
       }
+      scalar_from = nvec * kVec;
     }
-#pragma unroll
-    for (int u = 0; u < kRound; ++u) {
-      if (len[u] == 0) continue;
-#pragma unroll
-      for (int k = 0; k < kVec; ++k) {
-        T gk = static_cast<T>(vg[u][k]);
-        if (has_scale) gk = o_mul(gk, scale);  // grad *= clip factor (optim.py:170)
-        op(vp[u][k], gk, v0[u][k], v1[u][k]);
-      }
-      const int t = own[u];
-      const int64_t e = off[u];
-      T* p = static_cast<T*>(mp.p[t]) + e;
-      G* g = static_cast<G*>(mp.g[t]) + e;
-      T* a = Op::kSlots >= 1 ? static_cast<T*>(mp.s0[t]) + e : nullptr;
-      T* b = Op::kSlots >= 2 ? static_cast<T*>(mp.s1[t]) + e : nullptr;
-      __nv_bfloat16* sh = shadow ? static_cast<__nv_bfloat16*>(mp.sh[t]) + e : nullptr;
-      if (len[u] == kVec && mp.vok[t]) {
-        st4(p, vp[u]);
-        if (Op::kSlots >= 1) st4s(a, v0[u]);
-        if (Op::kSlots >= 2) st4s(b, v1[u]);
-        if (zero_grad) st4_zero(g);
-        if (shadow) st4_bf16(sh, vp[u]);
-      } else {
-#pragma unroll
-        for (int k = 0; k < kVec; ++k) {
-          if (k >= len[u]) break;
-          p[k] = vp[u][k];
-          if (Op::kSlots >= 1) a[k] = v0[u][k];
-          if (Op::kSlots >= 2) b[k] = v1[u][k];
-          if (zero_grad) st1_zero(g + k);
-          if (shadow) sh[k] = __float2bfloat16_rn(static_cast<float>(vp[u][k]));
-        }
-      }
+    for (int e = scalar_from + threadIdx.x; e < len; e += kThreads) {
+      T pv = p[e];
+      T a = Op::kSlots >= 1 ? s0[e] : T(0);
+      T b = Op::kSlots >= 2 ? s1[e] : T(0);
+      T gk = static_cast<T>(ld1(g + e));
+      if (has_scale) gk = o_mul(gk, scale);
+      op(pv, gk, a, b);
+      p[e] = pv;
+      if (Op::kSlots >= 1) s0[e] = a;
+      if (Op::kSlots >= 2) s1[e] = b;
+      if (zero_grad) st1_zero(g + e);
+      if (shadow) sh[e] = __float2bfloat16_rn(static_cast<float>(pv));
     }
   }
 }
@@ -536,83 +482,26 @@ int64_t pack(const of_tensor_list* l, int first, int count, MTParams<CAP>& mp, i
   return tiles;
 }
 
-// Packs tensors [first, first+count) into a step parameter block; returns the
-// number of vector slots (0 if the list holds no elements).
-template <class T, class G, int CAP>
-int64_t pack_step(const of_tensor_list* l, int first, int count, StepParams<CAP>& mp, bool shadow) {
-  int64_t slots = 0;
-  mp.count = count;
-  for (int i = 0; i < count; ++i) {
-    const int k = first + i;
-    mp.p[i] = l->param[k];
-    mp.g[i] = l->grad[k];
-    mp.s0[i] = l->state0 ? l->state0[k] : nullptr;
-    mp.s1[i] = l->state1 ? l->state1[k] : nullptr;
-    mp.sh[i] = (shadow && l->shadow) ? l->shadow[k] : nullptr;
-    mp.n[i] = l->numel[k];
-    slots += (l->numel[k] + kVec - 1) / kVec;
-    mp.vend[i] = static_cast<int32_t>(slots < INT32_MAX ? slots : INT32_MAX);
-    mp.vok[i] = aligned(mp.p[i], 4 * sizeof(T)) && aligned(mp.g[i], 4 * sizeof(G)) &&
-                (!mp.s0[i] || aligned(mp.s0[i], 4 * sizeof(T))) &&
-                (!mp.s1[i] || aligned(mp.s1[i], 4 * sizeof(T))) &&
-                (!mp.sh[i] || aligned(mp.sh[i], 8));
-  }
-  return slots;
-}
-
-// Resident CTAs per SM of one kernel instantiation (occupancy query, once).
-template <class Op, class T, class G, int CAP, int UNR>
-int resident_ctas() {
-  static int cached = 0;
-  if (cached == 0) {
-    int nb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, mt_step_kernel<Op, T, G, CAP, UNR>,
-                                                      kThreads, 0) != cudaSuccess || nb < 1)
-      nb = 1;
-    cached = nb;
-  }
-  return cached;
-}
-
-// Tensors of one launch: as many as the parameter block holds while the slot
-// count stays within int32 (a single tensor beyond 2^33 elements is refused).
-inline int launch_span(const of_tensor_list* l, int first, int cap) {
-  int64_t slots = 0;
-  int c = 0;
-  while (first + c < l->n && c < cap) {
-    const int64_t s = (l->numel[first + c] + kVec - 1) / kVec;
-    if (slots + s > INT32_MAX - 2 * kThreads) break;
-    slots += s;
-    ++c;
-  }
-  return c;
-}
-
 template <class Op, class T, class G, int CAP>
 int launch_step_chunk(const of_tensor_list* l, int first, int count, const Op& op,
                       const void* gscale, uint32_t flags, const StepSrc& step, int max_ctas,
                       cudaStream_t s) {
   constexpr int U = Tune<G>::kUnr;
-  StepParams<CAP> mp;
-  const int64_t slots = pack_step<T, G, CAP>(l, first, count, mp, (flags & OF_FLAG_SHADOW_BF16) != 0);
-  if (slots == 0) return OF_OK;
-  // Lists of up to ~1 vector per resident thread: the 1-vector build (more
-  // resident CTAs, every slot in the first round); larger lists: U vectors of
-  // every stream in flight per thread.
-  const int sms = sm_count();
-  const int64_t small_res = static_cast<int64_t>(sms) * resident_ctas<Op, T, G, CAP, 1>();
-  const bool small = slots <= small_res * kThreads * OF_SMALL_SLOTS;
-  int64_t grid = small ? small_res : static_cast<int64_t>(sms) * resident_ctas<Op, T, G, CAP, U>();
-  if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
-  const int64_t need = (slots + kThreads - 1) / kThreads;  // at least one slot per thread
-  if (grid > need) grid = need;
-  if (grid < 1) grid = 1;
-  mp.per_cta = static_cast<int32_t>((slots + grid - 1) / grid);
-  grid = (slots + mp.per_cta - 1) / mp.per_cta;
-  if (small)
-    mt_step_kernel<Op, T, G, CAP, 1><<<static_cast<int>(grid), kThreads, 0, s>>>(mp, op, gscale, flags, step);
-  else
-    mt_step_kernel<Op, T, G, CAP, U><<<static_cast<int>(grid), kThreads, 0, s>>>(mp, op, gscale, flags, step);
+  MTParams<CAP> mp;
+  int64_t tiles = pack<CAP>(l, first, count, mp, kThreads * kVec * U);
+  if (tiles == 0) return OF_OK;
+  int64_t cap = static_cast<int64_t>(sm_count()) * kCtasPerSm;
+  if (max_ctas > 0 && max_ctas < cap) cap = max_ctas;
+  if (tiles < 2 * static_cast<int64_t>(sm_count()) && max_ctas == 0) {
+    // small launch: 1024-element tiles, 4x the CTAs for the same bytes
+    tiles = pack<CAP>(l, first, count, mp, kThreads * kVec);
+    const int grid = static_cast<int>(tiles < cap ? tiles : cap);
+    mt_step_kernel<Op, T, G, CAP, 1><<<grid, kThreads, 0, s>>>(mp, op, gscale, flags, step);
+    return check_launch("mt_step_kernel");
+  }
+  if (tiles > INT32_MAX) return fail(OF_ERR_INVALID, "tensor list too large for one launch");
+  const int grid = static_cast<int>(tiles < cap ? tiles : cap);
+  mt_step_kernel<Op, T, G, CAP, U><<<grid, kThreads, 0, s>>>(mp, op, gscale, flags, step);
   return check_launch("mt_step_kernel");
 }
 
@@ -621,19 +510,25 @@ int launch_step(const of_tensor_list* l, const Op& op, const void* gscale, uint3
                 const StepSrc& step, int max_ctas, cudaStream_t s) {
   int first = 0;
   while (first < l->n) {
-    // up to 256 tensors in one launch: a ~14 KB parameter block (CUDA >= 12.1
-    // accepts up to 32 KB), so a whole CNN's parameter set is one kernel
-    const int c = launch_span(l, first, kCapMax);
-    if (c == 0)
-      return fail(OF_ERR_INVALID, "tensor %d (%lld elements) too large for one launch", first,
-                  (long long)l->numel[first]);
+    const int left = l->n - first;
     int st;
-    if (c <= 4) st = launch_step_chunk<Op, T, G, 4>(l, first, c, op, gscale, flags, step, max_ctas, s);
-    else if (c <= 16) st = launch_step_chunk<Op, T, G, 16>(l, first, c, op, gscale, flags, step, max_ctas, s);
-    else if (c <= 64) st = launch_step_chunk<Op, T, G, 64>(l, first, c, op, gscale, flags, step, max_ctas, s);
-    else st = launch_step_chunk<Op, T, G, kCapMax>(l, first, c, op, gscale, flags, step, max_ctas, s);
+    if (left <= 4) {
+      st = launch_step_chunk<Op, T, G, 4>(l, first, left, op, gscale, flags, step, max_ctas, s);
+      first += left;
+    } else if (left <= 16) {
+      st = launch_step_chunk<Op, T, G, 16>(l, first, left, op, gscale, flags, step, max_ctas, s);
+      first += left;
+    } else if (left <= 64) {
+      st = launch_step_chunk<Op, T, G, 64>(l, first, left, op, gscale, flags, step, max_ctas, s);
+      first += left;
+    } else {
+      // up to 256 tensors in one launch: a 13 KB parameter block (CUDA >= 12.1
+      // accepts up to 32 KB), so a whole CNN's parameter set is one kernel
+      const int c = left < kCapMax ? left : kCapMax;
+      st = launch_step_chunk<Op, T, G, kCapMax>(l, first, c, op, gscale, flags, step, max_ctas, s);
+      first += c;
+    }
     if (st != OF_OK) return st;
-    first += c;
   }
   return OF_OK;
 }

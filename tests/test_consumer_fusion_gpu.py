@@ -120,7 +120,10 @@ def test_consumer_weights_follow_the_fp64_product():
         # the gradient bound, plus a few ulp of theta for the roundings.
         gerr = tokens * 2.0 ** -24 * gabs + np.spacing(np.abs(gref))
         slope = h.eta * h.epsilon / (np.abs(gref).astype(np.float64) + h.epsilon) ** 2
-        tol = 4 * np.spacing(np.abs(th)).astype(np.float64) + slope * gerr
+        # (the roundings are those of theta_old + delta: ulps of the larger
+        # operand, not of a result that cancels towards zero)
+        mag = np.maximum(np.abs(before[pid].cpu().numpy().reshape(-1)), np.float32(h.eta))
+        tol = 4 * np.spacing(mag).astype(np.float64) + slope * gerr
         err = np.abs(got.astype(np.float64) - th.astype(np.float64))
         bad = err > tol
         assert not bad.any(), (g.parameters[pid].name, int(bad.sum()), float(err[bad].max()),

@@ -1,0 +1,28 @@
+# round-2 session-3 pass B: ncu evidence for the slot-space update kernel
+mkdir -p gpurun_out
+# launch list of the headline's timed region (headline arm only)
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --replay-mode application --nvtx --nvtx-include "timed" -c 3000 --csv \
+  --log-file gpurun_out/launches.csv python bench.py --headline-only --steps 4 --warmup 3 --instances 1 > gpurun_out/ncu_bench.log 2>&1; echo ncu_list=$?
+# full sections of the update launches: in situ (bf buckets) and one pass over each parameter set
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:mt_step -s 15 -c 3 -o gpurun_out/prof_bf -f python tools/profile_kernels.py bf > gpurun_out/ncu_bf.log 2>&1; echo ncu_bf=$?
+for w in c2full vgg bert r50mixed; do
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:mt_step -s 2 -c 1 -o gpurun_out/prof_$w -f python tools/profile_kernels.py $w > gpurun_out/ncu_$w.log 2>&1; echo ncu_$w=$?
+done
+for r in gpurun_out/prof_*.ncu-rep; do
+  [ -f "$r" ] || continue
+  ncu -i "$r" --page raw --csv > "${r%.ncu-rep}.raw.csv" 2>/dev/null
+  ncu -i "$r" --page details --csv > "${r%.ncu-rep}.details.csv" 2>/dev/null
+  ncu -i "$r" --page source --csv > "${r%.ncu-rep}.source.csv" 2>/dev/null
+  rm -f "$r"
+done
+ls -la gpurun_out | tail -30
+for tool in memcheck racecheck synccheck initcheck; do
+  timeout 900 compute-sanitizer --tool $tool --print-limit 50 python tools/sanitize_kernels.py > gpurun_out/sanitizer_$tool.log 2>&1; echo sanitizer_$tool=$?
+  tail -2 gpurun_out/sanitizer_$tool.log
+done
+TORCH_CUDA_SANITIZER=1 timeout 900 python tools/csan_schedules.py > gpurun_out/csan.log 2>&1; echo csan=$?
+tail -3 gpurun_out/csan.log
+if [ -z "${SKIP_EXTRAS}" ]; then
+timeout 2400 python bench.py --extras c1,c3,c4,c5 --sweep 32,64,256,512 --extras-out gpurun_out/bench_extras_full.json > gpurun_out/bench_full.log 2> gpurun_out/bench_full.err; echo bench_full=$?
+tail -c 1600 gpurun_out/bench_full.log; tail -3 gpurun_out/bench_full.err
+fi

@@ -4,6 +4,7 @@
     python tools/profile_kernels.py vgg     # one multi-tensor Adam launch over VGG-16 (138 M params)
     python tools/profile_kernels.py bert    # one AdamW launch over BERT-base (206 tensors, 110 M)
     python tools/profile_kernels.py r50mixed  # ResNet-50 bf16 + fp32 masters, AdamW, one launch
+    python tools/profile_kernels.py c2full  # one SGD-momentum launch over MobileNetV2 (158 tensors, 2.24 M)
 """
 
 import sys
@@ -52,5 +53,9 @@ def r50mixed(iters=3):
     vgg(iters, "resnet50", "adamw", mixed=True)
 
 
+def c2full(iters=3):
+    vgg(iters, "mobilenet_v2_cifar", "sgd-momentum")
+
+
 if __name__ == "__main__":
-    {"bf": bf, "vgg": vgg, "bert": bert, "r50mixed": r50mixed}[sys.argv[1]]()
+    {"bf": bf, "vgg": vgg, "bert": bert, "r50mixed": r50mixed, "c2full": c2full}[sys.argv[1]]()
