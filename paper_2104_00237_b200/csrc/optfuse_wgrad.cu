@@ -16,10 +16,17 @@
 // GEMM (dX = dY W).  The caller issues that GEMM first on the same stream, so
 // every read of the old W precedes the update in stream order.
 //
-// Kernel (one 128 x BN output tile per CTA, 192 threads, warp-specialised):
+// Kernel (one 128 x BN output tile per cluster of S CTAs, 192 threads per CTA,
+// warp-specialised):
+//   split-K    the S CTAs of a cluster (S = 1, 2 or 4: enough CTAs to fill the
+//              SMs when the layer has few output tiles, e.g. 36 for 768 x 768)
+//              each accumulate 1/S of the tokens; after a cluster barrier every
+//              CTA sends the rows it does not own to their owner's shared
+//              memory (DSMEM), and each owner sums the S partials in rank order
+//              and updates its rows -- the gradient still never reaches HBM;
 //   warp 0     TMA producer: dY and X tiles (bf16, row-major [tokens][features],
-//              i.e. MN-major operands) into a kStages-deep smem ring, 128B
-//              swizzle, completion counted on an mbarrier per stage;
+//              i.e. MN-major operands) into a kStages-deep smem ring (6-8
+//              stages, ~190 KB), 128B swizzle, completion on an mbarrier per stage;
 //   warp 1     allocates TMEM (BN fp32 columns x 128 lanes) and one elected
 //              lane issues tcgen05.mma.cta_group::1.kind::f16 (M=128, N=BN,
 //              K=16 per instruction) into the TMEM accumulator, releasing each
@@ -33,6 +40,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cooperative_groups.h>
 #include <cstring>
 
 #include "../../include/optfuse_b200.h"
@@ -43,18 +51,23 @@ using namespace ofk;
 
 constexpr int kBM = 128;          // UMMA_M: TMEM lane = output row
 constexpr int kBK = 64;           // tokens per stage (one 128-byte swizzle row per token)
-constexpr int kStages = 4;
 constexpr int kWThreads = 192;    // warp 0 TMA, warp 1 MMA, warps 2..5 epilogue
 constexpr int kBox = 64;          // features per TMA box (64 bf16 = 128 B, the swizzle span)
+constexpr int kMaxSplit = 4;      // CTAs per cluster (split-K ways)
 
 template <int BN>
 struct Layout {
   static constexpr int kA = kBM * kBK * 2;          // dY tile, bytes
   static constexpr int kB = BN * kBK * 2;           // X tile, bytes
   static constexpr int kStage = kA + kB;
+  // the deepest ring that fits ~190 KB: 8 x 24 KB (BN 64), 6 x 32 KB (BN 128)
+  static constexpr int kStages = 196608 / kStage;
   static constexpr int kBoxBytes = kBox * kBK * 2;  // one [kBK][64] box = the MN stride (LBO)
   static constexpr int kSmem = kStages * kStage + 1024 /* 1024-B alignment slack */;
   static constexpr uint32_t kTmemCols = BN;         // power of two >= 32
+  // epilogue staging (reuses the ring once every CTA's MMAs are done): S slots
+  // of 128/S rows, i.e. always 128 padded rows of fp32
+  static_assert(kBM * (BN + 4) * 4 <= kStages * kStage, "epilogue staging exceeds the ring");
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -167,6 +180,7 @@ wgrad_step_kernel(const __grid_constant__ CUtensorMap map_dy, const __grid_const
                   const WgradParams wp, const Op op_in, const StepSrc step) {
   using L = Layout<BN>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
+  constexpr int kStages = L::kStages;
   __shared__ __align__(8) uint64_t full[kStages];
   __shared__ __align__(8) uint64_t empty[kStages];
   __shared__ __align__(8) uint64_t acc_full;
@@ -179,6 +193,12 @@ wgrad_step_kernel(const __grid_constant__ CUtensorMap map_dy, const __grid_const
   const int m0 = blockIdx.y * kBM;
   const int n0 = blockIdx.x * BN;
   const int kblocks = (wp.T + kBK - 1) / kBK;
+  // split-K: this CTA's token blocks [kb0, kb1) (the host keeps every split non-empty)
+  const int S = static_cast<int>(gridDim.z);
+  const int rank = static_cast<int>(blockIdx.z);
+  const int kb_per = (kblocks + S - 1) / S;
+  const int kb0 = rank * kb_per;
+  const int kb1 = kb0 + kb_per < kblocks ? kb0 + kb_per : kblocks;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -202,9 +222,10 @@ wgrad_step_kernel(const __grid_constant__ CUtensorMap map_dy, const __grid_const
     if (lane == 0) {   // ===== TMA producer =====
       asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(&map_dy)) : "memory");
       asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(&map_x)) : "memory");
-      for (int kb = 0; kb < kblocks; ++kb) {
-        const int s = kb % kStages;
-        mbar_wait(&empty[s], ((kb / kStages) & 1) ^ 1);
+      for (int kb = kb0; kb < kb1; ++kb) {
+        const int i = kb - kb0;
+        const int s = i % kStages;
+        mbar_wait(&empty[s], ((i / kStages) & 1) ^ 1);
         unsigned char* a = smem + s * L::kStage;
         unsigned char* b = a + L::kA;
         mbar_expect_tx(&full[s], L::kStage);
@@ -219,9 +240,10 @@ wgrad_step_kernel(const __grid_constant__ CUtensorMap map_dy, const __grid_const
   } else if (warp == 1) {
     if (lane == 0) {   // ===== MMA issuer =====
       constexpr uint32_t idesc = umma_idesc_bf16_mn<BN>();
-      for (int kb = 0; kb < kblocks; ++kb) {
-        const int s = kb % kStages;
-        mbar_wait(&full[s], (kb / kStages) & 1);
+      for (int kb = kb0; kb < kb1; ++kb) {
+        const int i = kb - kb0;
+        const int s = i % kStages;
+        mbar_wait(&full[s], (i / kStages) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t a = smem_u32(smem + s * L::kStage);
         const uint32_t b = a + L::kA;
@@ -229,56 +251,119 @@ wgrad_step_kernel(const __grid_constant__ CUtensorMap map_dy, const __grid_const
         for (int k = 0; k < kBK / 16; ++k) {   // 16 tokens = 16 swizzle rows = 2048 B
           const uint64_t da = umma_desc_mn_sw128(a + k * 2048, L::kBoxBytes, 1024);
           const uint64_t db = umma_desc_mn_sw128(b + k * 2048, L::kBoxBytes, 1024);
-          umma_bf16(tmem, da, db, idesc, (kb | k) != 0);
+          umma_bf16(tmem, da, db, idesc, (i | k) != 0);
         }
         umma_commit(&empty[s]);                 // stage free once these MMAs have read it
       }
       umma_commit(&acc_full);                   // accumulator complete
     }
-  } else {
-    // ===== epilogue: one output row per thread, 32 columns per TMEM load =====
+  }
+  // ===== epilogue =====
+  // 1. every epilogue warp copies its 32-lane TMEM quarter (this CTA's partial
+  //    of 32 rows) into the shared memory of the quarter's owner -- its own
+  //    CTA unless split -- as [slot = rank][owned row][BN + 4 padding] fp32
+  //    (16-byte rows: the 128-bit stores of 8 rows and the 128-bit loads of
+  //    one row both hit 32 distinct banks);
+  // 2. barrier (cluster-wide when split): all partials delivered;
+  // 3. the owner's 128 epilogue threads sum each owned element's S partials in
+  //    rank order and apply the update to 4 consecutive columns per thread, so
+  //    the theta / history / shadow rows move as coalesced runs of BN * 4 bytes.
+  constexpr int kPitch = BN + 4;
+  const int q = warp & 3;                        // TMEM lane quarter this warp may access
+  const int owner = (q * S) >> 2;                // the cluster rank that updates quarter q
+  const int rows_owned = kBM / S;
+  float* recv = reinterpret_cast<float*>(smem);  // the ring is free once the MMAs are done
+  if (warp >= 2) {
+    mbar_wait(&acc_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  }
+  __syncwarp();
+  namespace cg = cooperative_groups;
+  if (S > 1) cg::this_cluster().sync();          // every ring in the cluster is free
+  if (warp >= 2) {
+    const int orow = (q - (owner * 4) / S) * 32 + lane;   // row within the owner's rows
+    float* base = recv + (static_cast<size_t>(rank) * rows_owned + orow) * kPitch;
+    float* dst = S > 1 ? cg::this_cluster().map_shared_rank(base, owner) : base;
+    const uint32_t tq = tmem + (static_cast<uint32_t>(q * 32) << 16);
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      float g[32];
+      tmem_ld_32x32b_x32(tq + c * 32, g);
+#pragma unroll
+      for (int j = 0; j < 32; j += 4)
+        *reinterpret_cast<float4*>(dst + c * 32 + j) = make_float4(g[j], g[j + 1], g[j + 2], g[j + 3]);
+    }
+  }
+  if (S > 1) cg::this_cluster().sync();          // partials delivered
+  else __syncthreads();
+  if (warp >= 2) {
     Op op = op_in;
     if (step.offset != nullptr) {
       int64_t t = step.t_base + *step.offset;
       t = t < 1 ? 1 : (t >= step.rows ? step.rows - 1 : t);
       op.set_step(step.table[2 * t], step.table[2 * t + 1]);
     }
-    const int q = warp & 3;                     // TMEM lane quarter this warp may access
-    const int row = q * 32 + lane;
-    const int m = m0 + row;
-    mbar_wait(&acc_full, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int et = threadIdx.x - 64;             // 0..127
+    constexpr int kQuads = BN / 4;               // float4 columns per row
+    constexpr int kRowsPerPass = 128 / kQuads;   // 4 (BN 128) or 8 (BN 64)
+    const int col = (et % kQuads) * 4;
+    const int n = n0 + col;
+    const int row_base = rank * rows_owned;      // first owned row of the tile
+    constexpr int R = 4;                         // rows in flight per thread: all loads first
+    float* __restrict__ P = wp.param;
+    float* __restrict__ A = wp.s0;
+    float* __restrict__ B = wp.s1;
 #pragma unroll 1
-    for (int c = 0; c < BN / 32; ++c) {
-      float g[32];
-      tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(q * 32) << 16) + c * 32, g);
-      const int n = n0 + c * 32;
-      if (m >= wp.M || n >= wp.N) continue;
-      const int64_t off = static_cast<int64_t>(m) * wp.N + n;
-      float* p = wp.param + off;
-      float* s0 = Op::kSlots >= 1 ? wp.s0 + off : nullptr;
-      float* s1 = Op::kSlots >= 2 ? wp.s1 + off : nullptr;
+    for (int r0 = et / kQuads; r0 < rows_owned; r0 += kRowsPerPass * R) {
+      float g[R][4], pp[R][4], aa[R][4], bb[R][4];
+      int64_t off[R];
+      bool ok[R];
 #pragma unroll
-      for (int j = 0; j < 32; j += 4) {
-        float4 pv = *reinterpret_cast<const float4*>(p + j);
-        float4 a = Op::kSlots >= 1 ? *reinterpret_cast<const float4*>(s0 + j) : make_float4(0, 0, 0, 0);
-        float4 b = Op::kSlots >= 2 ? *reinterpret_cast<const float4*>(s1 + j) : make_float4(0, 0, 0, 0);
-        float pp[4] = {pv.x, pv.y, pv.z, pv.w}, aa[4] = {a.x, a.y, a.z, a.w}, bb[4] = {b.x, b.y, b.z, b.w};
+      for (int u = 0; u < R; ++u) {
+        const int r = r0 + u * kRowsPerPass;
+        const int m = m0 + row_base + r;
+        ok[u] = r < rows_owned && m < wp.M && n < wp.N;
+        off[u] = static_cast<int64_t>(m) * wp.N + n;
+        if (!ok[u]) continue;
+        const float4 g4 = *reinterpret_cast<const float4*>(recv + static_cast<size_t>(r) * kPitch + col);
+        g[u][0] = g4.x; g[u][1] = g4.y; g[u][2] = g4.z; g[u][3] = g4.w;
+        for (int k = 1; k < S; ++k) {            // the S partials in rank order
+          const float4 h = *reinterpret_cast<const float4*>(
+              recv + (static_cast<size_t>(k) * rows_owned + r) * kPitch + col);
+          g[u][0] = __fadd_rn(g[u][0], h.x);
+          g[u][1] = __fadd_rn(g[u][1], h.y);
+          g[u][2] = __fadd_rn(g[u][2], h.z);
+          g[u][3] = __fadd_rn(g[u][3], h.w);
+        }
+        const float4 pv = *reinterpret_cast<const float4*>(P + off[u]);
+        pp[u][0] = pv.x; pp[u][1] = pv.y; pp[u][2] = pv.z; pp[u][3] = pv.w;
+        if (Op::kSlots >= 1) {
+          const float4 a = *reinterpret_cast<const float4*>(A + off[u]);
+          aa[u][0] = a.x; aa[u][1] = a.y; aa[u][2] = a.z; aa[u][3] = a.w;
+        }
+        if (Op::kSlots >= 2) {
+          const float4 b = *reinterpret_cast<const float4*>(B + off[u]);
+          bb[u][0] = b.x; bb[u][1] = b.y; bb[u][2] = b.z; bb[u][3] = b.w;
+        }
+      }
 #pragma unroll
-        for (int e = 0; e < 4; ++e) op(pp[e], g[j + e], aa[e], bb[e]);
-        *reinterpret_cast<float4*>(p + j) = make_float4(pp[0], pp[1], pp[2], pp[3]);
-        if (Op::kSlots >= 1) *reinterpret_cast<float4*>(s0 + j) = make_float4(aa[0], aa[1], aa[2], aa[3]);
-        if (Op::kSlots >= 2) *reinterpret_cast<float4*>(s1 + j) = make_float4(bb[0], bb[1], bb[2], bb[3]);
+      for (int u = 0; u < R; ++u) {
+        if (!ok[u]) continue;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) op(pp[u][e], g[u][e], aa[u][e], bb[u][e]);
+        *reinterpret_cast<float4*>(P + off[u]) = make_float4(pp[u][0], pp[u][1], pp[u][2], pp[u][3]);
+        if (Op::kSlots >= 1) *reinterpret_cast<float4*>(A + off[u]) = make_float4(aa[u][0], aa[u][1], aa[u][2], aa[u][3]);
+        if (Op::kSlots >= 2) *reinterpret_cast<float4*>(B + off[u]) = make_float4(bb[u][0], bb[u][1], bb[u][2], bb[u][3]);
         if (wp.shadow) {
-          __nv_bfloat162 lo = __floats2bfloat162_rn(pp[0], pp[1]);
-          __nv_bfloat162 hi = __floats2bfloat162_rn(pp[2], pp[3]);
-          uint2 u;
-          u.x = *reinterpret_cast<uint32_t*>(&lo);
-          u.y = *reinterpret_cast<uint32_t*>(&hi);
-          *reinterpret_cast<uint2*>(wp.shadow + off + j) = u;
+          __nv_bfloat162 lo = __floats2bfloat162_rn(pp[u][0], pp[u][1]);
+          __nv_bfloat162 hi = __floats2bfloat162_rn(pp[u][2], pp[u][3]);
+          uint2 w;
+          w.x = *reinterpret_cast<uint32_t*>(&lo);
+          w.y = *reinterpret_cast<uint32_t*>(&hi);
+          *reinterpret_cast<uint2*>(wp.shadow + off[u]) = w;
         }
         if (wp.grad_out)
-          *reinterpret_cast<float4*>(wp.grad_out + off + j) = make_float4(g[j], g[j + 1], g[j + 2], g[j + 3]);
+          *reinterpret_cast<float4*>(wp.grad_out + off[u]) = make_float4(g[u][0], g[u][1], g[u][2], g[u][3]);
       }
     }
   }
@@ -320,7 +405,7 @@ int make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t cols) {
 
 template <class Op, int BN>
 int launch_wgrad(const CUtensorMap& mdy, const CUtensorMap& mx, const WgradParams& wp, const Op& op,
-                 const StepSrc& step, cudaStream_t s) {
+                 const StepSrc& step, int split, cudaStream_t s) {
   using L = Layout<BN>;
   static bool configured = false;
   if (!configured) {
@@ -329,8 +414,20 @@ int launch_wgrad(const CUtensorMap& mdy, const CUtensorMap& mx, const WgradParam
       return fail(OF_ERR_CUDA, "cudaFuncSetAttribute(wgrad smem %d)", L::kSmem);
     configured = true;
   }
-  const dim3 grid((wp.N + BN - 1) / BN, (wp.M + kBM - 1) / kBM);
-  wgrad_step_kernel<Op, BN><<<grid, kWThreads, L::kSmem, s>>>(mdy, mx, wp, op, step);
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3((wp.N + BN - 1) / BN, (wp.M + kBM - 1) / kBM, split);
+  cfg.blockDim = dim3(kWThreads);
+  cfg.dynamicSmemBytes = L::kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = split;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, wgrad_step_kernel<Op, BN>, mdy, mx, wp, op, step);
   return check_launch("wgrad_step_kernel");
 }
 
@@ -391,11 +488,16 @@ extern "C" int of_wgrad_step(const of_wgrad_args* a, const of_hparams* hp, uint3
                            ? StepSrc{hp->step_offset_dev, hp->step_table_dev, hp->step_table_rows, hp->t_base}
                            : StepSrc{nullptr, nullptr, 0, 0};
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  // 128-wide tiles when they already fill the SMs, else 64-wide (twice the CTAs)
-  const int64_t tiles128 = ((wp.M + kBM - 1) / kBM) * ((wp.N + 127) / 128);
-  const bool wide = tiles128 >= sm_count() && wp.N % 128 == 0;
+  // 128-wide tiles where the columns allow; split-K across a cluster of 2 or 4
+  // CTAs while that still fits the SMs and leaves each split >= 4 token blocks
+  const bool wide = wp.N % 128 == 0;
+  const int bn = wide ? 128 : 64;
+  const int64_t tiles = static_cast<int64_t>((wp.M + kBM - 1) / kBM) * ((wp.N + bn - 1) / bn);
+  const int kblocks = (wp.T + kBK - 1) / kBK;
+  int split = 1;
+  while (split < kMaxSplit && tiles * split * 2 <= sm_count() && kblocks >= 4 * split * 2) split *= 2;
   return with_op<float>(hp, [&](auto op) {
-    return wide ? launch_wgrad<decltype(op), 128>(mdy, mx, wp, op, step, s)
-                : launch_wgrad<decltype(op), 64>(mdy, mx, wp, op, step, s);
+    return wide ? launch_wgrad<decltype(op), 128>(mdy, mx, wp, op, step, split, s)
+                : launch_wgrad<decltype(op), 64>(mdy, mx, wp, op, step, split, s);
   });
 }

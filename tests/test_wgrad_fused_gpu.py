@@ -22,8 +22,11 @@ from oracle import optim_ref
 pytestmark = pytest.mark.gpu
 DEV = "cuda"
 
-SHAPES = [(768, 768, 4096), (3072, 768, 4096), (768, 3072, 4096),   # BERT-base Linear (M, N, T)
-          (136, 96, 200), (128, 64, 64), (264, 160, 1000)]
+# BERT-base Linear (M, N, T): 768 x 768 runs as a 4-way split-K cluster, the
+# FFN shapes unsplit; then ragged token/row/column tails, unsplit (136 x 96,
+# 128 x 64), 4-way (264 x 160 x 1000) and 2-way (256 x 128 x 512) splits
+SHAPES = [(768, 768, 4096), (3072, 768, 4096), (768, 3072, 4096),
+          (136, 96, 200), (128, 64, 64), (264, 160, 1000), (256, 128, 512), (256, 256, 4096)]
 
 
 def _problem(M, N, T, seed=0, slots=2):
@@ -61,7 +64,7 @@ def test_gradient_matches_fp64_product(M, N, T):
 
 
 @pytest.mark.parametrize("kind", ["adamw", "adam", "sgd-momentum", "sgd"])
-@pytest.mark.parametrize("M,N,T", SHAPES[:2] + SHAPES[3:5])
+@pytest.mark.parametrize("M,N,T", SHAPES[:2] + SHAPES[3:7])
 def test_fused_update_bitwise_vs_multi_tensor_kernel(kind, M, N, T):
     """Same gradient, same functor: the epilogue's update equals of_policy_step_mt."""
     slots = {"sgd": 0, "sgd-momentum": 1}.get(kind, 2)
