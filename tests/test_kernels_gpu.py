@@ -273,16 +273,17 @@ def test_spec_kats_on_gpu(spec_kats):
     assert p.value.detach().cpu().tolist() == spec_kats["weight_decay"]["theta"]
 
 
-@pytest.mark.parametrize("max_ctas", [1, 7, 49])
-def test_capped_grid_same_bits(max_ctas):
-    """A capped grid (background update on the side stream) walks the same
-    tiles with fewer CTAs: identical results."""
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("max_ctas", [1, 7, 49, 148])
+def test_capped_grid_same_bits(max_ctas, dtype):
+    """A capped grid (background update on the side stream: 64-thread CTAs,
+    each walking its share of the tiles) gives identical results."""
     rng = np.random.default_rng(max_ctas)
     sizes = [3, 4097, 300001, 77]
-    ps = [torch.from_numpy(rng.standard_normal(n).astype(np.float32)).to(DEV) for n in sizes]
-    gs = [torch.from_numpy(rng.standard_normal(n).astype(np.float32)).to(DEV) for n in sizes]
-    ms = [torch.zeros(n, device=DEV) for n in sizes]
-    vs = [torch.zeros(n, device=DEV) for n in sizes]
+    ps = [torch.from_numpy(rng.standard_normal(n).astype(dtype)).to(DEV) for n in sizes]
+    gs = [torch.from_numpy(rng.standard_normal(n).astype(dtype)).to(DEV) for n in sizes]
+    ms = [torch.zeros(n, device=DEV, dtype=ps[0].dtype) for n in sizes]
+    vs = [torch.zeros(n, device=DEV, dtype=ps[0].dtype) for n in sizes]
     ref = [(p.cpu().numpy().copy(), g.cpu().numpy().copy()) for p, g in zip(ps, gs)]
     tl = _raw_list(ps, gs, ms, vs)
     hp = kernels.hparams("adam", 1e-3, 0.9, 1e-4, 1e-8, 0.9, 0.999, 0.9, 1, max_ctas=max_ctas)

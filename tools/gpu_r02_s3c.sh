@@ -19,3 +19,8 @@ python -c "
 import json;d=json.load(open('gpurun_out/bench_extras_c5m.json'))
 for s,r in d['c5m']['schedules'].items(): print('%-60s %8.3f %s'%(s,r['ms_per_step'],r.get('speedup_vs_ours_unfused','')))"
 fi
+# residency of the C3 / C5 backward kernels (room for a co-resident update CTA?)
+for cfg in c3 c5; do
+timeout 900 ncu --metrics gpu__time_duration.sum,launch__grid_size,launch__block_size,launch__registers_per_thread,launch__shared_mem_per_block_static,launch__shared_mem_per_block_dynamic,launch__occupancy_limit_registers,launch__occupancy_limit_shared_mem,launch__occupancy_limit_warps,launch__occupancy_limit_blocks,launch__waves_per_multiprocessor \
+  --clock-control none --nvtx --nvtx-include "iter" -c 5000 --csv --log-file gpurun_out/residency_$cfg.csv python tools/iter_dram.py $cfg baseline > gpurun_out/residency_$cfg.log 2>&1; echo residency_$cfg=$?
+done
