@@ -235,11 +235,8 @@ template <> struct Tune<__nv_bfloat16> {
 // One multi-tensor policy step.  T: param/state type; G: grad type; UNR:
 // vectors per thread per tile (tile = 256 * 4 * UNR elements).  Small lists
 // use UNR=1 so that even a few MB spread over more CTAs than there are SMs.
-// NT: threads per CTA -- 256, or 64 for a capped launch (max_ctas > 0) meant
-// to run beside other kernels: a 64-thread CTA needs 6-8 K registers, so it
-// fits next to a kernel that leaves only part of an SM free.
-template <class Op, class T, class G, int CAP, int UNR, int NT = kThreads>
-__global__ void __launch_bounds__(NT, NT == kThreads ? Tune<G>::kMinBlocks : 1)
+template <class Op, class T, class G, int CAP, int UNR>
+__global__ void __launch_bounds__(kThreads, Tune<G>::kMinBlocks)
 mt_step_kernel(const __grid_constant__ MTParams<CAP> mp, const Op op_in,
                const void* __restrict__ gscale, uint32_t flags, const StepSrc step) {
   using GV = typename GradVal<G>::type;
@@ -249,7 +246,7 @@ mt_step_kernel(const __grid_constant__ MTParams<CAP> mp, const Op op_in,
     t = t < 1 ? 1 : (t >= step.rows ? step.rows - 1 : t);
     op.set_step(step.table[2 * t], step.table[2 * t + 1]);
   }
-  constexpr int kTileU = NT * kVec * UNR;
+  constexpr int kTileU = kThreads * kVec * UNR;
   constexpr int kRoundMax = sizeof(T) == 8 ? 2 : 4;
   constexpr int kRound = UNR < kRoundMax ? UNR : kRoundMax;  // vectors in flight per thread
   const int total = mp.tile_end[mp.count - 1];
@@ -281,7 +278,7 @@ mt_step_kernel(const __grid_constant__ MTParams<CAP> mp, const Op op_in,
         GV vg[kRound][4];
 #pragma unroll
         for (int u = 0; u < kRound; ++u) {
-          const int j = threadIdx.x + (r + u) * NT;
+          const int j = threadIdx.x + (r + u) * kThreads;
           if (j < nvec) {
             ld4(p + 4 * j, vp[u]);
             ld4s(g + 4 * j, vg[u]);
@@ -291,7 +288,7 @@ mt_step_kernel(const __grid_constant__ MTParams<CAP> mp, const Op op_in,
         }
 #pragma unroll
         for (int u = 0; u < kRound; ++u) {
-          const int j = threadIdx.x + (r + u) * NT;
+          const int j = threadIdx.x + (r + u) * kThreads;
           if (j < nvec) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
@@ -309,7 +306,7 @@ mt_step_kernel(const __grid_constant__ MTParams<CAP> mp, const Op op_in,
       }
       scalar_from = nvec * kVec;
     }
-    for (int e = scalar_from + threadIdx.x; e < len; e += NT) {
+    for (int e = scalar_from + threadIdx.x; e < len; e += kThreads) {
       T pv = p[e];
       T a = Op::kSlots >= 1 ? s0[e] : T(0);
       T b = Op::kSlots >= 2 ? s1[e] : T(0);
@@ -493,17 +490,9 @@ int launch_step_chunk(const of_tensor_list* l, int first, int count, const Op& o
   MTParams<CAP> mp;
   int64_t tiles = pack<CAP>(l, first, count, mp, kThreads * kVec * U);
   if (tiles == 0) return OF_OK;
-  if (max_ctas > 0) {
-    // capped: 64-thread CTAs, each walking its share of 64 x 4 x U-element tiles
-    constexpr int kNarrow = 64;
-    tiles = pack<CAP>(l, first, count, mp, kNarrow * kVec * U);
-    if (tiles > INT32_MAX) return fail(OF_ERR_INVALID, "tensor list too large for one launch");
-    const int grid = static_cast<int>(tiles < max_ctas ? tiles : max_ctas);
-    mt_step_kernel<Op, T, G, CAP, U, kNarrow><<<grid, kNarrow, 0, s>>>(mp, op, gscale, flags, step);
-    return check_launch("mt_step_kernel");
-  }
-  const int64_t cap = static_cast<int64_t>(sm_count()) * kCtasPerSm;
-  if (tiles < 2 * static_cast<int64_t>(sm_count())) {
+  int64_t cap = static_cast<int64_t>(sm_count()) * kCtasPerSm;
+  if (max_ctas > 0 && max_ctas < cap) cap = max_ctas;
+  if (tiles < 2 * static_cast<int64_t>(sm_count()) && max_ctas == 0) {
     // small launch: 1024-element tiles, 4x the CTAs for the same bytes
     tiles = pack<CAP>(l, first, count, mp, kThreads * kVec);
     const int grid = static_cast<int>(tiles < cap ? tiles : cap);

@@ -416,17 +416,27 @@ int launch_wgrad(const CUtensorMap& mdy, const CUtensorMap& mx, const WgradParam
   }
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof(cfg));
-  cfg.gridDim = dim3((wp.N + BN - 1) / BN, (wp.M + kBM - 1) / kBM, split);
-  cfg.blockDim = dim3(kWThreads);
-  cfg.dynamicSmemBytes = L::kSmem;
-  cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 1;
   attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = split;
+  cfg.blockDim = dim3(kWThreads);
+  cfg.dynamicSmemBytes = L::kSmem;
+  cfg.stream = s;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  const int tiles = ((wp.N + BN - 1) / BN) * ((wp.M + kBM - 1) / kBM);
+  // every cluster must be resident at once (one CTA per SM, clusters confined
+  // to a GPC): halve the split until the tiles' clusters fit in one wave
+  for (; split > 1; split /= 2) {
+    attr[0].val.clusterDim.z = split;
+    cfg.gridDim = dim3((wp.N + BN - 1) / BN, (wp.M + kBM - 1) / kBM, split);
+    int fit = 0;
+    if (cudaOccupancyMaxActiveClusters(&fit, wgrad_step_kernel<Op, BN>, &cfg) == cudaSuccess && tiles <= fit)
+      break;
+  }
+  attr[0].val.clusterDim.z = split;
+  cfg.gridDim = dim3((wp.N + BN - 1) / BN, (wp.M + kBM - 1) / kBM, split);
   cudaLaunchKernelEx(&cfg, wgrad_step_kernel<Op, BN>, mdy, mx, wp, op, step);
   return check_launch("wgrad_step_kernel");
 }

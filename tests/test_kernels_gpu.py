@@ -276,8 +276,8 @@ def test_spec_kats_on_gpu(spec_kats):
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
 @pytest.mark.parametrize("max_ctas", [1, 7, 49, 148])
 def test_capped_grid_same_bits(max_ctas, dtype):
-    """A capped grid (background update on the side stream: 64-thread CTAs,
-    each walking its share of the tiles) gives identical results."""
+    """A capped grid (background update on the side stream) walks the same
+    tiles with fewer CTAs: identical results."""
     rng = np.random.default_rng(max_ctas)
     sizes = [3, 4097, 300001, 77]
     ps = [torch.from_numpy(rng.standard_normal(n).astype(dtype)).to(DEV) for n in sizes]

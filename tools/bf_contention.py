@@ -31,11 +31,9 @@ def main():
     W = bench.WORKLOADS[wl]
     arms = [("baseline", "baseline", {})]
     for bucket, tag in ((1 << 20, "1M"), (0, "layer")):
-        # cap 0: full-size CTAs filling the GPU; cap > 0: that many 64-thread
-        # CTAs, small enough to sit beside the backward's kernels
-        for cap in (0, 74, 148, 296, 592):
+        for cap in (0, 8, 16, 32, 74):
             for prio in ("high", "low"):
-                if prio == "low" and cap not in (0, 148):
+                if prio == "low" and cap not in (0, 16):
                     continue
                 kw = dict(workers=2, bucket_elems=bucket, update_ctas=cap, update_priority=prio)
                 arms.append((f"bf_{tag}_cap{cap}_{prio}", "backward-fusion", kw))

@@ -1,4 +1,4 @@
-# round-2 session-3 pass B: ncu evidence for the slot-space update kernel
+# round-2 session-3 pass B: ncu evidence for the update kernel, sanitizers, contention, full extras
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?; tail -1 gpurun_out/smoke.log
 timeout 600 python -m pytest -q -m gpu tests/test_consumer_fusion_gpu.py tests/test_kernels_gpu.py > gpurun_out/pytest_b.log 2>&1; echo pytest_b=$?; tail -2 gpurun_out/pytest_b.log

@@ -24,3 +24,7 @@ for cfg in c3 c5; do
 timeout 900 ncu --metrics gpu__time_duration.sum,launch__grid_size,launch__block_size,launch__registers_per_thread,launch__shared_mem_per_block_static,launch__shared_mem_per_block_dynamic,launch__occupancy_limit_registers,launch__occupancy_limit_shared_mem,launch__occupancy_limit_warps,launch__occupancy_limit_blocks,launch__waves_per_multiprocessor \
   --clock-control none --nvtx --nvtx-include "iter" -c 5000 --csv --log-file gpurun_out/residency_$cfg.csv python tools/iter_dram.py $cfg baseline > gpurun_out/residency_$cfg.log 2>&1; echo residency_$cfg=$?
 done
+timeout 900 python -m pytest -q -m gpu tests/test_kernels_gpu.py -k capped > gpurun_out/pytest_capped.log 2>&1; echo pytest_capped=$?; tail -1 gpurun_out/pytest_capped.log
+for c in ${CONTENTION:-c3 c5 c4}; do timeout 1500 python tools/bf_contention.py $c 3 > gpurun_out/bf_narrow_$c.json 2> gpurun_out/bf_narrow_$c.err; echo narrow_$c=$?; python -c "
+import json,sys; d=json.load(open('gpurun_out/bf_narrow_$c.json'))
+for k,v in list(d.values())[0].items(): print(k, v['median_ms'], v['vs_baseline'])" ; done
