@@ -16,7 +16,7 @@
 // GEMM (dX = dY W).  The caller issues that GEMM first on the same stream, so
 // every read of the old W precedes the update in stream order.
 //
-// Kernel (one 128 x BN output tile per cluster of S CTAs, 192 threads per CTA,
+// Kernel (one 128 x BN output tile per cluster of S CTAs, 320 threads per CTA,
 // warp-specialised):
 //   split-K    the S CTAs of a cluster (S = 1, 2 or 4: enough CTAs to fill the
 //              SMs when the layer has few output tiles, e.g. 36 for 768 x 768)
@@ -31,9 +31,12 @@
 //              lane issues tcgen05.mma.cta_group::1.kind::f16 (M=128, N=BN,
 //              K=16 per instruction) into the TMEM accumulator, releasing each
 //              smem stage with tcgen05.commit;
-//   warps 2-5  epilogue: tcgen05.ld 32 columns of their 32 TMEM lanes (one
-//              output row per thread), then theta/history loads, the update
-//              functor, stores of theta/history/bf16 shadow.
+//   warps 2-9  epilogue: during the mainloop, bulk L2 prefetches of the owned
+//              theta/history rows; then tcgen05.ld of their TMEM lane quarter
+//              (two warps per quarter, half the columns each) into the owner's
+//              shared memory, and the update over the owned rows, 4 columns per
+//              thread (8 warps: the update's division/square-root chains need
+//              the warps to hide their latency).
 // D[m][n] = sum_t dY[t][m] * X[t][n]  (= dW of y = x W^T, W: [out=M][in=N]).
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -51,9 +54,19 @@ using namespace ofk;
 
 constexpr int kBM = 128;          // UMMA_M: TMEM lane = output row
 constexpr int kBK = 64;           // tokens per stage (one 128-byte swizzle row per token)
-constexpr int kWThreads = 192;    // warp 0 TMA, warp 1 MMA, warps 2..5 epilogue
+constexpr int kEpiThreads = 256;  // 8 epilogue warps: enough to hide the update's latency chains
+constexpr int kWThreads = 64 + kEpiThreads;   // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
 constexpr int kBox = 64;          // features per TMA box (64 bf16 = 128 B, the swizzle span)
-constexpr int kMaxSplit = 4;      // CTAs per cluster (split-K ways)
+#ifndef OFW_MAX_SPLIT
+#define OFW_MAX_SPLIT 4
+#endif
+#ifndef OFW_RING_BYTES
+#define OFW_RING_BYTES 196608
+#endif
+#ifndef OFW_NO_UPDATE   // 1: probe builds skip the epilogue's global traffic (mainloop timing)
+#define OFW_NO_UPDATE 0
+#endif
+constexpr int kMaxSplit = OFW_MAX_SPLIT;   // CTAs per cluster (split-K ways)
 
 template <int BN>
 struct Layout {
@@ -61,7 +74,7 @@ struct Layout {
   static constexpr int kB = BN * kBK * 2;           // X tile, bytes
   static constexpr int kStage = kA + kB;
   // the deepest ring that fits ~190 KB: 8 x 24 KB (BN 64), 6 x 32 KB (BN 128)
-  static constexpr int kStages = 196608 / kStage;
+  static constexpr int kStages = OFW_RING_BYTES / kStage;
   static constexpr int kBoxBytes = kBox * kBK * 2;  // one [kBK][64] box = the MN stride (LBO)
   static constexpr int kSmem = kStages * kStage + 1024 /* 1024-B alignment slack */;
   static constexpr uint32_t kTmemCols = BN;         // power of two >= 32
@@ -265,7 +278,7 @@ wgrad_step_kernel(const __grid_constant__ CUtensorMap map_dy, const __grid_const
   //    (16-byte rows: the 128-bit stores of 8 rows and the 128-bit loads of
   //    one row both hit 32 distinct banks);
   // 2. barrier (cluster-wide when split): all partials delivered;
-  // 3. the owner's 128 epilogue threads sum each owned element's S partials in
+  // 3. the owner's 256 epilogue threads sum each owned element's S partials in
   //    rank order and apply the update to 4 consecutive columns per thread, so
   //    the theta / history / shadow rows move as coalesced runs of BN * 4 bytes.
   constexpr int kPitch = BN + 4;
@@ -274,6 +287,22 @@ wgrad_step_kernel(const __grid_constant__ CUtensorMap map_dy, const __grid_const
   const int rows_owned = kBM / S;
   float* recv = reinterpret_cast<float*>(smem);  // the ring is free once the MMAs are done
   if (warp >= 2) {
+    // While the tensor cores run, pull this CTA's owned rows of theta and
+    // history into L2 (one bulk prefetch per row and stream), so the update
+    // below reads them from L2 instead of waiting on HBM after the mainloop.
+    if (!OFW_NO_UPDATE) {
+      const int et = threadIdx.x - 64;
+      const int ncols = (n0 + BN <= wp.N ? BN : wp.N - n0);
+      for (int r = et; r < rows_owned * 3; r += kEpiThreads) {
+        const int m = m0 + rank * rows_owned + r / 3;
+        if (m >= wp.M || ncols <= 0) continue;
+        const int which = r % 3;
+        const float* base = which == 0 ? wp.param : which == 1 ? wp.s0 : wp.s1;
+        if (base == nullptr) continue;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                     :: "l"(base + static_cast<int64_t>(m) * wp.N + n0), "r"(ncols * 4) : "memory");
+      }
+    }
     mbar_wait(&acc_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   }
@@ -285,8 +314,9 @@ wgrad_step_kernel(const __grid_constant__ CUtensorMap map_dy, const __grid_const
     float* base = recv + (static_cast<size_t>(rank) * rows_owned + orow) * kPitch;
     float* dst = S > 1 ? cg::this_cluster().map_shared_rank(base, owner) : base;
     const uint32_t tq = tmem + (static_cast<uint32_t>(q * 32) << 16);
+    const int half = (warp - 2) >> 2;           // two warps per lane quarter split the columns
 #pragma unroll 1
-    for (int c = 0; c < BN / 32; ++c) {
+    for (int c = half; c < BN / 32; c += 2) {
       float g[32];
       tmem_ld_32x32b_x32(tq + c * 32, g);
 #pragma unroll
@@ -303,9 +333,9 @@ wgrad_step_kernel(const __grid_constant__ CUtensorMap map_dy, const __grid_const
       t = t < 1 ? 1 : (t >= step.rows ? step.rows - 1 : t);
       op.set_step(step.table[2 * t], step.table[2 * t + 1]);
     }
-    const int et = threadIdx.x - 64;             // 0..127
+    const int et = threadIdx.x - 64;             // 0 .. kEpiThreads - 1
     constexpr int kQuads = BN / 4;               // float4 columns per row
-    constexpr int kRowsPerPass = 128 / kQuads;   // 4 (BN 128) or 8 (BN 64)
+    constexpr int kRowsPerPass = kEpiThreads / kQuads;   // 8 (BN 128) or 16 (BN 64)
     const int col = (et % kQuads) * 4;
     const int n = n0 + col;
     const int row_base = rank * rows_owned;      // first owned row of the tile
@@ -322,7 +352,7 @@ wgrad_step_kernel(const __grid_constant__ CUtensorMap map_dy, const __grid_const
       for (int u = 0; u < R; ++u) {
         const int r = r0 + u * kRowsPerPass;
         const int m = m0 + row_base + r;
-        ok[u] = r < rows_owned && m < wp.M && n < wp.N;
+        ok[u] = r < rows_owned && m < wp.M && n < wp.N && !OFW_NO_UPDATE;
         off[u] = static_cast<int64_t>(m) * wp.N + n;
         if (!ok[u]) continue;
         const float4 g4 = *reinterpret_cast<const float4*>(recv + static_cast<size_t>(r) * kPitch + col);
