@@ -16,7 +16,7 @@
 // GEMM (dX = dY W).  The caller issues that GEMM first on the same stream, so
 // every read of the old W precedes the update in stream order.
 //
-// Kernel (one 128 x BN output tile per cluster of S CTAs, 320 threads per CTA,
+// Kernel (one 128 x BN output tile per cluster of S CTAs, 448 threads per CTA,
 // warp-specialised):
 //   split-K    the S CTAs of a cluster (S = 1, 2 or 4: enough CTAs to fill the
 //              SMs when the layer has few output tiles, e.g. 36 for 768 x 768)
@@ -31,11 +31,11 @@
 //              lane issues tcgen05.mma.cta_group::1.kind::f16 (M=128, N=BN,
 //              K=16 per instruction) into the TMEM accumulator, releasing each
 //              smem stage with tcgen05.commit;
-//   warps 2-9  epilogue: during the mainloop, bulk L2 prefetches of the owned
+//   warps 2-13 epilogue: during the mainloop, bulk L2 prefetches of the owned
 //              theta/history rows; then tcgen05.ld of their TMEM lane quarter
-//              (two warps per quarter, half the columns each) into the owner's
+//              (three warps per quarter, a third of the columns each) into the owner's
 //              shared memory, and the update over the owned rows, 4 columns per
-//              thread (8 warps: the update's division/square-root chains need
+//              thread (12 warps: the update's division/square-root chains need
 //              the warps to hide their latency).
 // D[m][n] = sum_t dY[t][m] * X[t][n]  (= dW of y = x W^T, W: [out=M][in=N]).
 #include <cuda.h>
@@ -54,8 +54,11 @@ using namespace ofk;
 
 constexpr int kBM = 128;          // UMMA_M: TMEM lane = output row
 constexpr int kBK = 64;           // tokens per stage (one 128-byte swizzle row per token)
-constexpr int kEpiThreads = 256;  // 8 epilogue warps: enough to hide the update's latency chains
-constexpr int kWThreads = 64 + kEpiThreads;   // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
+#ifndef OFW_EPI_WARPS
+#define OFW_EPI_WARPS 12
+#endif
+constexpr int kEpiThreads = 32 * OFW_EPI_WARPS;  // 12 epilogue warps: enough to hide the update's latency chains
+constexpr int kWThreads = 64 + kEpiThreads;   // warp 0 TMA, warp 1 MMA, warps 2.. epilogue
 constexpr int kBox = 64;          // features per TMA box (64 bf16 = 128 B, the swizzle span)
 #ifndef OFW_MAX_SPLIT
 #define OFW_MAX_SPLIT 4
@@ -278,7 +281,7 @@ wgrad_step_kernel(const __grid_constant__ CUtensorMap map_dy, const __grid_const
   //    (16-byte rows: the 128-bit stores of 8 rows and the 128-bit loads of
   //    one row both hit 32 distinct banks);
   // 2. barrier (cluster-wide when split): all partials delivered;
-  // 3. the owner's 256 epilogue threads sum each owned element's S partials in
+  // 3. the owner's 384 epilogue threads sum each owned element's S partials in
   //    rank order and apply the update to 4 consecutive columns per thread, so
   //    the theta / history / shadow rows move as coalesced runs of BN * 4 bytes.
   constexpr int kPitch = BN + 4;
@@ -314,9 +317,10 @@ wgrad_step_kernel(const __grid_constant__ CUtensorMap map_dy, const __grid_const
     float* base = recv + (static_cast<size_t>(rank) * rows_owned + orow) * kPitch;
     float* dst = S > 1 ? cg::this_cluster().map_shared_rank(base, owner) : base;
     const uint32_t tq = tmem + (static_cast<uint32_t>(q * 32) << 16);
-    const int half = (warp - 2) >> 2;           // two warps per lane quarter split the columns
+    constexpr int kPerQuarter = kEpiThreads / 128;   // warps per lane quarter: they split the columns
+    const int half = (warp - 2) >> 2;
 #pragma unroll 1
-    for (int c = half; c < BN / 32; c += 2) {
+    for (int c = half; c < BN / 32; c += kPerQuarter) {
       float g[32];
       tmem_ld_32x32b_x32(tq + c * 32, g);
 #pragma unroll
@@ -335,7 +339,7 @@ wgrad_step_kernel(const __grid_constant__ CUtensorMap map_dy, const __grid_const
     }
     const int et = threadIdx.x - 64;             // 0 .. kEpiThreads - 1
     constexpr int kQuads = BN / 4;               // float4 columns per row
-    constexpr int kRowsPerPass = kEpiThreads / kQuads;   // 8 (BN 128) or 16 (BN 64)
+    constexpr int kRowsPerPass = kEpiThreads / kQuads;   // 12 (BN 128) or 24 (BN 64)
     const int col = (et % kQuads) * 4;
     const int n = n0 + col;
     const int row_base = rank * rows_owned;      // first owned row of the tile
