@@ -462,12 +462,17 @@ int launch_wgrad(const CUtensorMap& mdy, const CUtensorMap& mx, const WgradParam
   const int tiles = ((wp.N + BN - 1) / BN) * ((wp.M + kBM - 1) / kBM);
   // every cluster must be resident at once (one CTA per SM, clusters confined
   // to a GPC): halve the split until the tiles' clusters fit in one wave
+  static int fit_cache[kMaxSplit + 1] = {0};   // resident clusters per split (queried once)
   for (; split > 1; split /= 2) {
     attr[0].val.clusterDim.z = split;
     cfg.gridDim = dim3((wp.N + BN - 1) / BN, (wp.M + kBM - 1) / kBM, split);
-    int fit = 0;
-    if (cudaOccupancyMaxActiveClusters(&fit, wgrad_step_kernel<Op, BN>, &cfg) == cudaSuccess && tiles <= fit)
-      break;
+    if (fit_cache[split] == 0) {
+      int fit = 0;
+      if (cudaOccupancyMaxActiveClusters(&fit, wgrad_step_kernel<Op, BN>, &cfg) != cudaSuccess || fit < 1)
+        fit = -1;
+      fit_cache[split] = fit;
+    }
+    if (tiles <= fit_cache[split]) break;
   }
   attr[0].val.clusterDim.z = split;
   cfg.gridDim = dim3((wp.N + BN - 1) / BN, (wp.M + kBM - 1) / kBM, split);
