@@ -53,6 +53,8 @@ _OPTIONS = (
     ("--device", "device", dict(default="cuda")),
     ("--dtype", "dtype", dict(default="fp32", choices=("fp32", "bf16"),
                               help="bf16: bf16 module with fp32 master weights (networks only)")),
+    ("--tf32", "tf32", dict(type=int, default=0,
+                            help="1: TF32 tensor cores for the networks' convolutions and matmuls")),
 )
 
 

@@ -71,6 +71,7 @@ class BenchConfig:
     grad_reset: str = "zero"
     device: str = "cuda"
     dtype: str = "fp32"
+    tf32: int = 0
 
     def __post_init__(self):
         checks = (
@@ -296,6 +297,17 @@ def run_bench(cfg: BenchConfig) -> dict:
     """Run one mode; returns its display lines, rows and the exit code."""
     handler = {"verify": _mode_verify, "trace": _mode_trace, "breakdown": _mode_breakdown,
                "sweep": _mode_sweep, "optimizers": _mode_optimizers, "time": _mode_time}[cfg.mode]
-    out = handler(cfg)
+    import torch
+    if not str(cfg.device).startswith("cuda"):
+        out = handler(cfg)
+    else:
+        # fp32 means fp32: no TF32 tensor-core rounding in the networks'
+        # convolutions and matmuls unless asked for (bench.py does the same)
+        prev = (torch.backends.cudnn.allow_tf32, torch.backends.cuda.matmul.allow_tf32)
+        torch.backends.cudnn.allow_tf32 = torch.backends.cuda.matmul.allow_tf32 = bool(cfg.tf32)
+        try:
+            out = handler(cfg)
+        finally:
+            torch.backends.cudnn.allow_tf32, torch.backends.cuda.matmul.allow_tf32 = prev
     out["mode"] = cfg.mode
     return out
