@@ -86,9 +86,6 @@ constexpr int kVec = 4;
 #ifndef OF_CS
 #define OF_CS 0
 #endif
-#ifndef OF_PDL   // 1: update launches overlap their launch with the predecessor's tail (PDL)
-#define OF_PDL 0
-#endif
 constexpr int kUnroll = OF_UNROLL;
 constexpr int kTile = kThreads * kVec * kUnroll;  // elements per tile
 constexpr int kCtasPerSm = 8;
@@ -243,11 +240,6 @@ __global__ void __launch_bounds__(kThreads, Tune<G>::kMinBlocks)
 mt_step_kernel(const __grid_constant__ MTParams<CAP> mp, const Op op_in,
                const void* __restrict__ gscale, uint32_t flags, const StepSrc step) {
   using GV = typename GradVal<G>::type;
-#if OF_PDL
-  // launched with programmatic stream serialization: everything the
-  // predecessor kernel wrote (e.g. the gradients) is visible after this
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-#endif
   Op op = op_in;
   if (step.offset != nullptr) {  // OF_FLAG_DEVICE_STEP: this replay's step index
     int64_t t = step.t_base + *step.offset;
@@ -490,26 +482,6 @@ int64_t pack(const of_tensor_list* l, int first, int count, MTParams<CAP>& mp, i
   return tiles;
 }
 
-template <class Op, class T, class G, int CAP, int UNR>
-void launch_mt(int grid, cudaStream_t s, const MTParams<CAP>& mp, const Op& op, const void* gscale,
-               uint32_t flags, const StepSrc& step) {
-#if OF_PDL
-  cudaLaunchConfig_t cfg;
-  memset(&cfg, 0, sizeof(cfg));
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, mt_step_kernel<Op, T, G, CAP, UNR>, mp, op, gscale, flags, step);
-#else
-  mt_step_kernel<Op, T, G, CAP, UNR><<<grid, kThreads, 0, s>>>(mp, op, gscale, flags, step);
-#endif
-}
-
 template <class Op, class T, class G, int CAP>
 int launch_step_chunk(const of_tensor_list* l, int first, int count, const Op& op,
                       const void* gscale, uint32_t flags, const StepSrc& step, int max_ctas,
@@ -524,12 +496,12 @@ int launch_step_chunk(const of_tensor_list* l, int first, int count, const Op& o
     // small launch: 1024-element tiles, 4x the CTAs for the same bytes
     tiles = pack<CAP>(l, first, count, mp, kThreads * kVec);
     const int grid = static_cast<int>(tiles < cap ? tiles : cap);
-    launch_mt<Op, T, G, CAP, 1>(grid, s, mp, op, gscale, flags, step);
+    mt_step_kernel<Op, T, G, CAP, 1><<<grid, kThreads, 0, s>>>(mp, op, gscale, flags, step);
     return check_launch("mt_step_kernel");
   }
   if (tiles > INT32_MAX) return fail(OF_ERR_INVALID, "tensor list too large for one launch");
   const int grid = static_cast<int>(tiles < cap ? tiles : cap);
-  launch_mt<Op, T, G, CAP, U>(grid, s, mp, op, gscale, flags, step);
+  mt_step_kernel<Op, T, G, CAP, U><<<grid, kThreads, 0, s>>>(mp, op, gscale, flags, step);
   return check_launch("mt_step_kernel");
 }
 
