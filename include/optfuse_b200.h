@@ -43,8 +43,9 @@ extern "C" {
 #endif
 
 /* ABI 3: grad_scale_dev of of_policy_step_mt is untyped (f32, or f64 with
- * OF_FLAG_SCALE_F64); of_mc_bucket carries dtypes; of_wgrad_step. */
-#define OF_ABI_VERSION 3
+ * OF_FLAG_SCALE_F64); of_mc_bucket carries dtypes; of_wgrad_step.
+ * ABI 4: of_dp_sqnorm_peer (global-norm clipping on the peer transport). */
+#define OF_ABI_VERSION 4
 
 typedef enum of_status {
   OF_OK = 0,
@@ -188,6 +189,18 @@ typedef struct of_peer_bucket {
  * after (all writes landed).  flags: 0 or OF_FLAG_DEVICE_STEP. */
 int of_dp_step_peer(const of_peer_bucket* bucket, const of_hparams* hp,
                     const float* grad_scale_dev, uint32_t flags, void* stream);
+
+/* Global-norm clipping for the peer transport (optim.py:151-172 under data
+ * parallel): Sum over this rank's shard of (Sum_w grad_w)^2 -- the peers'
+ * gradients summed in rank order exactly as of_dp_step_peer sums them --
+ * accumulated in f64 with a fixed reduction order into *out_dev (added to it
+ * when accumulate != 0).  The caller all-reduces the scalar over the ranks and
+ * turns it into the clip factor with of_clip_coef.  Same barrier contract as
+ * of_dp_step_peer (every peer's gradients complete); workspace as
+ * of_sqnorm_mt.  Only world, rank, grad_dtype, peer_grad, shard_begin and
+ * shard_len of the bucket are read. */
+int of_dp_sqnorm_peer(const of_peer_bucket* bucket, double* workspace_dev, int64_t workspace_len,
+                      double* out_dev, int accumulate, void* stream);
 
 /* EXPERIMENTAL (not used by the data-parallel host layer; its numerics have
  * not run on a multi-GPU box yet).

@@ -22,7 +22,7 @@ OF_FLAG_ZERO_GRAD = 0x1
 OF_FLAG_SHADOW_BF16 = 0x2
 OF_FLAG_DEVICE_STEP = 0x4
 OF_FLAG_SCALE_F64 = 0x8
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 # of_kind (optim.py:22 minus newton, plus adamw)
 KIND_CODES = {"sgd": 0, "sgd-momentum": 1, "adagrad": 2, "rmsprop": 3, "adadelta": 4,
@@ -32,7 +32,7 @@ KIND_CODES = {"sgd": 0, "sgd-momentum": 1, "adagrad": 2, "rmsprop": 3, "adadelta
 SYMBOLS = ("of_abi_version", "of_status_string", "of_last_error", "of_launch_count",
            "of_policy_step_mt", "of_sgdm_mt", "of_adam_mt", "of_step_advance", "of_dp_step_peer",
            "of_sqnorm_workspace_len", "of_sqnorm_mt", "of_clip_coef", "of_exact_matmul",
-           "of_copy_mt", "of_dp_step_multicast", "of_wgrad_step")
+           "of_copy_mt", "of_dp_step_multicast", "of_wgrad_step", "of_dp_sqnorm_peer")
 
 _vp = ctypes.c_void_p
 _PP = ctypes.POINTER(ctypes.c_void_p)
@@ -121,6 +121,9 @@ def lib():
     so.of_dp_step_peer.restype = ctypes.c_int
     so.of_dp_step_peer.argtypes = [ctypes.POINTER(OfPeerBucket), ctypes.POINTER(OfHparams), _vp,
                                    ctypes.c_uint32, _vp]
+    so.of_dp_sqnorm_peer.restype = ctypes.c_int
+    so.of_dp_sqnorm_peer.argtypes = [ctypes.POINTER(OfPeerBucket), _vp, ctypes.c_int64, _vp,
+                                     ctypes.c_int, _vp]
     so.of_dp_step_multicast.restype = ctypes.c_int
     so.of_dp_step_multicast.argtypes = [ctypes.POINTER(OfMcBucket), ctypes.POINTER(OfHparams), _vp,
                                         ctypes.c_uint32, _vp]

@@ -615,6 +615,45 @@ peer_step_kernel(const __grid_constant__ PeerParams pp, const Op op_in,
   }
 }
 
+// Sum of squares of the peer-summed gradient shard (of_dp_sqnorm_peer): the
+// same rank-order sum as peer_step_kernel, squared and accumulated in f64;
+// per-CTA partials in a fixed order, then sqnorm_finalize_kernel.
+template <class G>
+__global__ void __launch_bounds__(kThreads)
+peer_sqnorm_kernel(const __grid_constant__ PeerParams pp, double* __restrict__ partials) {
+  using GV = typename GradVal<G>::type;
+  const int64_t nvec = pp.len / kVec;
+  const int W = pp.world;
+  double acc2 = 0.0;
+  for (int64_t v = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; v < nvec;
+       v += static_cast<int64_t>(gridDim.x) * kThreads) {
+    const int64_t e = pp.begin + kVec * v;
+    GV acc[4], tmp[4];
+    ld4(static_cast<const G*>(pp.grad[0]) + e, acc);
+    for (int w = 1; w < W; ++w) {
+      ld4(static_cast<const G*>(pp.grad[w]) + e, tmp);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc[k] = o_add(acc[k], tmp[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const double x = static_cast<double>(acc[k]);
+      acc2 = __dadd_rn(acc2, __dmul_rn(x, x));
+    }
+  }
+  __shared__ double red[kThreads / 32];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc2 = __dadd_rn(acc2, __shfl_down_sync(0xffffffffu, acc2, off));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc2;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < kThreads / 32 ? red[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v = __dadd_rn(v, __shfl_down_sync(0xffffffffu, v, off));
+    if (threadIdx.x == 0) partials[blockIdx.x] = v;
+  }
+}
+
 template <class T, class G, bool kMixed>
 int dispatch_peer(const PeerParams& pp, const of_hparams* hp, const float* gscale, uint32_t flags,
                   cudaStream_t s) {
@@ -954,6 +993,53 @@ int of_dp_step_peer(const of_peer_bucket* b, const of_hparams* hp, const float* 
   if (b->param_dtype == OF_F32) return dispatch_peer<float, float, false>(pp, hp, grad_scale_dev, flags, s);
   if (b->param_dtype == OF_F64) return dispatch_peer<double, double, false>(pp, hp, grad_scale_dev, flags, s);
   return fail(OF_ERR_UNSUPPORTED, "param dtype %d", b->param_dtype);
+}
+
+int of_dp_sqnorm_peer(const of_peer_bucket* b, double* workspace_dev, int64_t workspace_len,
+                      double* out_dev, int accumulate, void* stream) {
+  g_err[0] = '\0';
+  if (!b) return fail(OF_ERR_INVALID, "bucket is NULL");
+  if (!workspace_dev || workspace_len < 1) return fail(OF_ERR_INVALID, "sqnorm needs a workspace");
+  if (!out_dev) return fail(OF_ERR_INVALID, "sqnorm output pointer is NULL");
+  if (b->world < 1 || b->world > OF_MAX_PEERS)
+    return fail(OF_ERR_INVALID, "world %d outside [1, %d]", b->world, OF_MAX_PEERS);
+  if (b->rank < 0 || b->rank >= b->world)
+    return fail(OF_ERR_INVALID, "rank %d outside [0, %d)", b->rank, b->world);
+  if (b->shard_begin < 0 || b->shard_len < 0 || (b->shard_begin % 4) || (b->shard_len % 4))
+    return fail(OF_ERR_INVALID, "shard [%lld, +%lld) must be non-negative multiples of 4",
+                (long long)b->shard_begin, (long long)b->shard_len);
+  if (!b->peer_grad) return fail(OF_ERR_INVALID, "peer gradient pointer array is NULL");
+  PeerParams pp;
+  memset(&pp, 0, sizeof(pp));
+  for (int w = 0; w < b->world; ++w) {
+    if (!b->peer_grad[w]) return fail(OF_ERR_INVALID, "peer %d has a NULL grad buffer", w);
+    pp.grad[w] = b->peer_grad[w];
+  }
+  pp.begin = b->shard_begin;
+  pp.len = b->shard_len;
+  pp.world = b->world;
+  pp.rank = b->rank;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t nvec = pp.len / kVec;
+  if (nvec == 0) {
+    if (!accumulate && cudaMemsetAsync(out_dev, 0, sizeof(double), s) != cudaSuccess)
+      return fail(OF_ERR_CUDA, "cudaMemsetAsync failed");
+    return OF_OK;
+  }
+  int64_t grid = (nvec + kThreads - 1) / kThreads;
+  int64_t cap = static_cast<int64_t>(sm_count()) * 4;
+  if (cap > workspace_len) cap = workspace_len;
+  if (grid > cap) grid = cap;
+  switch (b->grad_dtype) {
+    case OF_F32: peer_sqnorm_kernel<float><<<static_cast<int>(grid), kThreads, 0, s>>>(pp, workspace_dev); break;
+    case OF_F64: peer_sqnorm_kernel<double><<<static_cast<int>(grid), kThreads, 0, s>>>(pp, workspace_dev); break;
+    case OF_BF16: peer_sqnorm_kernel<__nv_bfloat16><<<static_cast<int>(grid), kThreads, 0, s>>>(pp, workspace_dev); break;
+    default: return fail(OF_ERR_UNSUPPORTED, "grad dtype %d", b->grad_dtype);
+  }
+  const int st = check_launch("peer_sqnorm_kernel");
+  if (st != OF_OK) return st;
+  sqnorm_finalize_kernel<<<1, kThreads, 0, s>>>(workspace_dev, static_cast<int>(grid), out_dev, accumulate);
+  return check_launch("sqnorm_finalize_kernel");
 }
 
 int of_dp_step_multicast(const of_mc_bucket* b, const of_hparams* hp, const float* grad_scale_dev,

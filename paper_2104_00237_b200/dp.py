@@ -32,6 +32,11 @@ its shard of the gradients over the peers, updates it, writes the result into
 every peer's flat_param and zeroes the gradient shard it read, between two
 cross-rank barriers.  No staging buffer, no reduce-scatter output, and the
 all-gather traffic is issued by the same threads that computed the values.
+Global-norm clipping on this transport: after a barrier, one kernel per bucket
+(``of_dp_sqnorm_peer``) sums the squares of the peer-summed gradient shard in
+f64 (the same rank-order sum the fused step uses), then the scalar is
+all-reduced and the factor folded into the steps' gradient scale, as on the
+NCCL transport.
 """
 
 from __future__ import annotations
@@ -192,9 +197,6 @@ class DataParallelFusion:
         # the sharded updates' device gradient scale
         self._clip_gscale = None
         self._host_factor = None
-        if policy.clip_norm is not None and transport == "peer":
-            raise ConfigError("global-norm clipping needs the reduce-scattered shards "
-                              "(transport='nccl'): the peer kernel sums and updates in one pass")
         if policy.clip_norm is not None and self.cuda:
             dev = self.device
             self._sq = torch.zeros((), dtype=torch.float64, device=dev)
@@ -203,6 +205,8 @@ class DataParallelFusion:
             self._clip_gscale = torch.zeros((), dtype=torch.float32, device=dev)
             self._ws = torch.empty(kernels.sqnorm_workspace_len(), dtype=torch.float64, device=dev)
             for b in self.buckets:
+                if transport == "peer":   # of_dp_sqnorm_peer reads the shard from every peer
+                    continue
                 tl = kernels.TensorList(1)
                 tl.set(0, None, b.grad_shard)
                 tl.set_dtypes(torch.float32 if self.mixed else b.grad_shard.dtype, b.grad_shard.dtype)
@@ -254,8 +258,29 @@ class DataParallelFusion:
             mx = self.policy.clip_norm
             self._host_factor = 1.0 if norm <= mx else mx / norm
             return
+        if self.transport == "peer":
+            # on the communication stream, like the peer steps (barrier order):
+            # barrier (every rank's gradients complete), then Σ over this rank's
+            # shard of the peer-summed gradient squared -- the same rank-order
+            # sum the fused step will use -- then the same all-reduce and factor
+            cur = torch.cuda.current_stream()
+            on_comm = cur == self.comm
+            if not on_comm:
+                self.comm.wait_stream(cur)
+            with torch.cuda.stream(self.comm):
+                self._sync.barrier(channel=0, timeout_ms=self.barrier_timeout_ms)
+                for i, b in enumerate(self.buckets):
+                    kernels.dp_sqnorm_peer(b.peer, self._ws, self._sq, i > 0, None)
+                self._finish_clip()
+            if not on_comm:
+                cur.wait_stream(self.comm)
+            return
         for i, b in enumerate(self.buckets):
             kernels.sqnorm(b.sq_tl, self._ws, self._sq, i > 0, None)
+        self._finish_clip()
+
+    def _finish_clip(self) -> None:
+        W = self.world
         dist.all_reduce(self._sq, group=self.group)
         self._sq.div_(float(W * W))
         kernels.clip_coef(self._sq, self.policy.clip_norm, self._coef, self._factor, None)
@@ -324,7 +349,7 @@ class DataParallelFusion:
                 self.comm.wait_stream(cur)
             with torch.cuda.stream(self.comm):
                 self._sync.barrier(channel=0, timeout_ms=self.barrier_timeout_ms)
-                kernels.dp_step_peer(b.peer, self.policy._hparams(t), self.scale,
+                kernels.dp_step_peer(b.peer, self.policy._hparams(t), self._gscale(),
                                      self.policy.device_step_flag, None)
                 self._sync.barrier(channel=0, timeout_ms=self.barrier_timeout_ms)
             if not on_comm:

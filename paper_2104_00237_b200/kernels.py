@@ -129,6 +129,15 @@ def dp_step_peer(pb: PeerBucket, hp: nat.OfHparams, grad_scale, flags: int, stre
         nat.check(st, "of_dp_step_peer")
 
 
+def dp_sqnorm_peer(pb: PeerBucket, workspace: torch.Tensor, out: torch.Tensor, accumulate: bool,
+                   stream) -> None:
+    """of_dp_sqnorm_peer: Σ over this rank's shard of the peer-summed gradient squared (f64)."""
+    st = nat.lib().of_dp_sqnorm_peer(pb.ref, workspace.data_ptr(), workspace.numel(), out.data_ptr(),
+                                     int(accumulate), _handle(stream))
+    if st:
+        nat.check(st, "of_dp_sqnorm_peer")
+
+
 class McBucket:
     """Host ``of_mc_bucket`` of one data-parallel bucket over NVLS multicast
     (multicast addresses of the flat gradient/parameter buffers, fixed)."""

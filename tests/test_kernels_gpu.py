@@ -357,6 +357,44 @@ def test_peer_step_simulated_ranks_on_one_gpu(world, kind, mixed):
             assert got.tobytes() == slots[name][r * S:(r + 1) * S].tobytes(), (r, name)
 
 
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+@pytest.mark.parametrize("mixed", [False, True])
+def test_peer_sqnorm_simulated_ranks_on_one_gpu(world, mixed):
+    """of_dp_sqnorm_peer with W "ranks" on this GPU: each rank's partial is
+    Σ over its shard of (Σ_w g_w)², the peers summed in rank order in the
+    gradient's compute type exactly as of_dp_step_peer sums them; the ranks'
+    partials add up to the numpy f64 value (reduction order: 1e-12), and
+    accumulate=1 adds to the output."""
+    rng = np.random.default_rng(world)
+    n = 4 * world * 1031
+    S = n // world
+    grads = [rng.standard_normal(n).astype(np.float32) for _ in range(world)]
+    if mixed:
+        grads = [torch.from_numpy(g).to(torch.bfloat16).float().numpy() for g in grads]
+        gbufs = [torch.from_numpy(g).to(DEV).to(torch.bfloat16) for g in grads]
+    else:
+        gbufs = [torch.from_numpy(g.copy()).to(DEV) for g in grads]
+    gsum = grads[0].copy()
+    for w in range(1, world):
+        gsum = np.add(gsum, grads[w])           # f32, rank order
+    ws = torch.empty(kernels.sqnorm_workspace_len(), dtype=torch.float64, device=DEV)
+    pdt = torch.bfloat16 if mixed else torch.float32
+    total = 0.0
+    for r in range(world):
+        out = torch.full((), 7.0, dtype=torch.float64, device=DEV)
+        pb = kernels.PeerBucket(world, r, pdt, pdt, [g.data_ptr() for g in gbufs],
+                                [g.data_ptr() for g in gbufs], None, None, None, r * S, S)
+        kernels.dp_sqnorm_peer(pb, ws, out, False, None)
+        want = float(np.sum(gsum[r * S:(r + 1) * S].astype(np.float64) ** 2))
+        assert abs(out.item() - want) <= 1e-12 * want, (r, out.item(), want)
+        kernels.dp_sqnorm_peer(pb, ws, out, True, None)     # accumulate
+        assert abs(out.item() - 2 * want) <= 2e-12 * want
+        total += want
+    assert total > 0
+    for w in range(world):   # the reduction only reads the gradients
+        assert torch.equal(gbufs[w].float().cpu(), torch.from_numpy(grads[w]))
+
+
 def test_copy_mt_many_tensors_any_alignment():
     """of_copy_mt: >256 tensors (two launches), odd byte counts and unaligned views."""
     torch.manual_seed(0)

@@ -30,7 +30,7 @@ def test_library_exports_every_symbol():
     so = nat.lib()
     for name in declared_symbols():
         assert hasattr(so, name), name
-    assert so.of_abi_version() == nat.ABI_VERSION == 3
+    assert so.of_abi_version() == nat.ABI_VERSION == 4
     assert so.of_status_string(0) == b"ok"
     assert so.of_sqnorm_workspace_len() >= 148
 
@@ -103,6 +103,19 @@ def test_invalid_arguments_rejected_before_launch():
     assert so.of_dp_step_peer(pb.ref, ctypes.byref(sgdm), None, 0, None) == nat.OF_ERR_INVALID
     assert so.of_dp_step_peer(pb.ref, ctypes.byref(sgdm), None, nat.OF_FLAG_ZERO_GRAD,
                               None) == nat.OF_ERR_INVALID
+    # ABI 4: the peer transport's clip reduction validates the same fields first
+    ws = 0x7000
+    assert so.of_dp_sqnorm_peer(None, ws, 16, 0x8000, 0, None) == nat.OF_ERR_INVALID
+    assert so.of_dp_sqnorm_peer(pb.ref, None, 0, 0x8000, 0, None) == nat.OF_ERR_INVALID
+    assert b"workspace" in so.of_last_error()
+    assert so.of_dp_sqnorm_peer(pb.ref, ws, 16, None, 0, None) == nat.OF_ERR_INVALID
+    pb.struct.rank = 5
+    assert so.of_dp_sqnorm_peer(pb.ref, ws, 16, 0x8000, 0, None) == nat.OF_ERR_INVALID
+    pb.struct.rank = 0
+    pb.struct.shard_begin = 2
+    assert so.of_dp_sqnorm_peer(pb.ref, ws, 16, 0x8000, 0, None) == nat.OF_ERR_INVALID
+    assert b"multiples of 4" in so.of_last_error()
+    pb.struct.shard_begin = 0
     # the (experimental) multicast step is fp32 only (ABI 3 dtype fields)
     mb = kernels.McBucket(1, 0, 0x1000, 0x2000, None, None, None, 0, 8, dtype=torch.bfloat16)
     mb.struct.local_param = 0x3000
