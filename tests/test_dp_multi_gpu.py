@@ -31,6 +31,9 @@ def test_data_parallel_across_gpus():
                 assert r["bitwise_vs_oracle"], (transport, sched, r)
             else:
                 assert r["max_rel_err"] <= 1e-6, (transport, sched, r)
+    for schedule in ("baseline+clip", "forward-fusion+clip"):
+        r = res[f"clip:{schedule}"]
+        assert r["ranks_agree"] and r["nccl_vs_peer_max_rel"] <= 1e-5, (schedule, r)
     for rank, r in res["multicast"].items():
         if isinstance(r, str):          # fabric without NVLS multicast
             assert r.startswith("skip"), r

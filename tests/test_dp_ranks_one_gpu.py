@@ -30,3 +30,6 @@ def test_data_parallel_real_ranks_one_gpu(world, mode):
     for sched in ("backward-fusion", "baseline", "forward-fusion"):
         assert res[sched]["ranks_agree"], sched
         assert res[sched]["bitwise_vs_oracle"], (sched, res[sched]["max_abs_err"])
+    for sched in ("baseline+clip", "forward-fusion+clip"):   # peer: of_dp_sqnorm_peer
+        assert res[sched]["ranks_agree"], sched
+        assert res[sched]["max_rel_err"] <= 1e-5, (sched, res[sched])

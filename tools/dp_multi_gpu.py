@@ -9,7 +9,10 @@ visible; it skips on the one-GPU boxes).
 * transport "peer": the fused of_dp_step_peer kernel over torch symmetric
   memory (peer loads/stores over NVLink), every schedule;
 * "multicast": of_dp_step_multicast (multimem.ld_reduce + multimem.st over an
-  NVLS multicast address of torch symmetric memory), when the fabric offers it.
+  NVLS multicast address of torch symmetric memory), when the fabric offers it;
+* "clip": baseline and forward fusion with global-norm clipping on both
+  transports (NCCL: sq-norm of the reduce-scattered shard; peer:
+  of_dp_sqnorm_peer), which must agree across ranks and with each other.
 
 Each rank trains the exact (fixed-order) chain model on its own inputs; every
 rank's parameters must equal the reference update (numpy oracle) applied to
@@ -35,6 +38,8 @@ import torch.multiprocessing as mp  # noqa: E402
 
 from dp_ranks_one_gpu import ETA, ITERS, KIND, LAYERS, WD, WIDTH, _inputs, _reference  # noqa: E402
 
+CLIP = 0.05   # small enough that every iteration clips
+
 
 def _worker(rank, world, port, transport, schedule, out):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -47,10 +52,11 @@ def _worker(rank, world, port, transport, schedule, out):
             out[rank] = _multicast(rank, world)
             return
         g = of.build_model("chain", layers=LAYERS, width=WIDTH, seed=0, device="cuda")
-        pol = of.OptimizerPolicy(KIND, eta=ETA, weight_decay=WD)
+        clip = schedule.endswith("+clip")
+        pol = of.OptimizerPolicy(KIND, eta=ETA, weight_decay=WD, clip_norm=CLIP if clip else None)
         dpf = DataParallelFusion(g, pol, bucket_elems=2 * WIDTH * WIDTH, transport=transport)
         run = {"backward-fusion": dpf.run_backward_fusion, "baseline": dpf.run_baseline,
-               "forward-fusion": dpf.run_forward_fusion}[schedule]
+               "forward-fusion": dpf.run_forward_fusion}[schedule.replace("+clip", "")]
         for x in _inputs(rank):
             run(torch.from_numpy(x).cuda())
         dpf.flush()
@@ -131,6 +137,21 @@ def main():
                 "ranks_agree": all(out[r] == out[0] for r in range(world)),
                 "bitwise_vs_oracle": out[0] == want.tobytes(),
                 "max_rel_err": float(np.max(np.abs(got - want) / np.maximum(np.abs(want), 1e-6)))}
+    # global-norm clipping (baseline / forward fusion): the two transports'
+    # norms differ only in the summation order
+    clip = {}
+    for transport in ("nccl", "peer"):
+        for schedule in ("baseline+clip", "forward-fusion+clip"):
+            out = mp.get_context("spawn").Manager().dict()
+            mp.start_processes(_worker, args=(world, _port(), transport, schedule, out),
+                               nprocs=world, join=True, start_method="spawn")
+            clip[(transport, schedule)] = (all(out[r] == out[0] for r in range(world)),
+                                           np.frombuffer(out[0], np.float32))
+    for schedule in ("baseline+clip", "forward-fusion+clip"):
+        a, b = clip[("nccl", schedule)], clip[("peer", schedule)]
+        res[f"clip:{schedule}"] = {
+            "ranks_agree": a[0] and b[0],
+            "nccl_vs_peer_max_rel": float(np.max(np.abs(a[1] - b[1]) / np.maximum(np.abs(a[1]), 1e-6)))}
     out = mp.get_context("spawn").Manager().dict()
     mp.start_processes(_worker, args=(world, _port(), "multicast", None, out), nprocs=world,
                        join=True, start_method="spawn")

@@ -8,7 +8,8 @@ with transport="peer", the of_dp_step_peer kernel reading and writing the
 other processes' buffers through their IPC mappings.  Each rank trains the
 exact (fixed-order) chain on its own input; every rank's parameters must
 equal the reference update applied to the rank-averaged gradient (numpy
-oracle), bit for bit.
+oracle), bit for bit; with global-norm clipping ("+clip") within 1e-5 (the
+norm's f64 reduction order).
 
     python tools/dp_ranks_one_gpu.py [W]        # prints one JSON line
 """
@@ -28,6 +29,7 @@ import torch.distributed as dist  # noqa: E402
 import torch.multiprocessing as mp  # noqa: E402
 
 KIND, ETA, WD, ITERS, LAYERS, WIDTH = "adam", 1e-2, 1e-3, 3, 4, 8
+CLIP = 0.05   # "+clip" schedules: small enough that every iteration clips
 
 
 def _inputs(rank):
@@ -76,10 +78,11 @@ def _worker(rank, world, port, schedule, out, transport="peer"):
 
         dp_mod.DataParallelFusion._symmetric = _ipc_symmetric
         g = of.build_model("chain", layers=LAYERS, width=WIDTH, seed=0, device="cuda")
-        pol = of.OptimizerPolicy(KIND, eta=ETA, weight_decay=WD)
+        clip = schedule.endswith("+clip")
+        pol = of.OptimizerPolicy(KIND, eta=ETA, weight_decay=WD, clip_norm=CLIP if clip else None)
         dpf = DataParallelFusion(g, pol, bucket_elems=2 * WIDTH * WIDTH, transport=transport)
         run = {"backward-fusion": dpf.run_backward_fusion, "baseline": dpf.run_baseline,
-               "forward-fusion": dpf.run_forward_fusion}[schedule]
+               "forward-fusion": dpf.run_forward_fusion}[schedule.replace("+clip", "")]
         for x in _inputs(rank):
             run(torch.from_numpy(x).cuda())
         dpf.flush()
@@ -90,7 +93,7 @@ def _worker(rank, world, port, schedule, out, transport="peer"):
         dist.destroy_process_group()
 
 
-def _reference(world):
+def _reference(world, clip=None):
     from oracle import chain_ref, optim_ref
     m = chain_ref.build("chain", layers=LAYERS, width=WIDTH, seed=0)
     h = optim_ref.Hyper(kind=KIND, eta=ETA, weight_decay=WD)
@@ -107,12 +110,19 @@ def _reference(world):
 
     for it in range(ITERS):
         grads = [grads_of(xs[r][it]) for r in range(world)]
-        for k, theta in enumerate(m.params):
+        avg = []
+        for k in range(len(m.params)):
             g = grads[0][k].copy()
             for r in range(1, world):
                 g = np.add(g, grads[r][k])
-            g = np.multiply(g, np.float32(1.0 / world))
-            optim_ref.step(KIND, h, theta, g, slots[k], it + 1)
+            avg.append(np.multiply(g, np.float32(1.0 / world)))
+        if clip is not None:   # optim.py:151-172 on the averaged gradient (norm in f64)
+            norm = float(np.sqrt(sum(float(np.dot(g.astype(np.float64), g.astype(np.float64)))
+                                     for g in avg)))
+            if norm > clip:
+                avg = [np.multiply(g, np.float32(clip / norm)) for g in avg]
+        for k, theta in enumerate(m.params):
+            optim_ref.step(KIND, h, theta, avg[k], slots[k], it + 1)
     return np.concatenate(m.params).tobytes()
 
 
@@ -122,7 +132,8 @@ def main():
     # collectives carried by the gloo group (NCCL refuses two ranks on one GPU)
     transport = "nccl" if len(sys.argv) > 2 and sys.argv[2] == "collectives" else "peer"
     res = {}
-    for schedule in ("backward-fusion", "baseline", "forward-fusion"):
+    for schedule in ("backward-fusion", "baseline", "forward-fusion", "baseline+clip",
+                     "forward-fusion+clip"):
         with socket.socket() as s:
             s.bind(("127.0.0.1", 0))
             port = s.getsockname()[1]
@@ -130,11 +141,12 @@ def main():
         mp.start_processes(_worker, args=(world, port, schedule, out, transport), nprocs=world,
                            join=True, start_method="spawn")
         same = all(out[r] == out[0] for r in range(world))
-        want = _reference(world)
+        want = _reference(world, CLIP if schedule.endswith("+clip") else None)
         got = np.frombuffer(out[0], np.float32)
         ref = np.frombuffer(want, np.float32)
         res[schedule] = {"ranks_agree": same, "bitwise_vs_oracle": out[0] == want,
-                         "max_abs_err": float(np.abs(got - ref).max())}
+                         "max_abs_err": float(np.abs(got - ref).max()),
+                         "max_rel_err": float(np.max(np.abs(got - ref) / np.maximum(np.abs(ref), 1e-6)))}
     print(json.dumps({"world": world, "transport": transport, **res}))
 
 
