@@ -38,6 +38,12 @@ def main():
                 kw = dict(workers=2, bucket_elems=bucket, update_ctas=cap, update_priority=prio)
                 arms.append((f"bf_{tag}_cap{cap}_{prio}", "backward-fusion", kw))
     arms.append(("bf_layer_inline", "backward-fusion", dict(workers=1, bucket_elems=0)))
+    if len(sys.argv) > 3 and sys.argv[3] == "inline":   # inline buckets vs the side stream only
+        arms = [("baseline", "baseline", {}),
+                ("bf_1M_cap0_high", "backward-fusion", dict(workers=2, bucket_elems=1 << 20)),
+                ("bf_layer_inline", "backward-fusion", dict(workers=1, bucket_elems=0)),
+                ("bf_1M_inline", "backward-fusion", dict(workers=1, bucket_elems=1 << 20)),
+                ("bf_4M_inline", "backward-fusion", dict(workers=1, bucket_elems=1 << 22))]
     instances = int(sys.argv[2]) if len(sys.argv) > 2 else 3
     res = {name: [] for name, _, _ in arms}
     for _ in range(instances):
