@@ -49,6 +49,25 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
+if int(os.environ.get("WORLD_SIZE", "1")) > 1 or "--force-dp" in sys.argv:
+    # NCCL reads its debug settings when the library loads (with torch), so
+    # they are set here, before any import of torch: rank 0's communicator
+    # lines (ranks, transport, NVLS) go to stdout ahead of the result line --
+    # the process group is destroyed before that line is printed -- and the
+    # other ranks stay quiet, so the result stays the last stdout line
+    # (the GPU image presets NCCL_DEBUG=VERSION, so a lower level is raised).
+    # NCCL writes them to a file that main() echoes before the result: NCCL
+    # logs once more while the process exits, after anything printed here.
+    if os.environ.get("RANK", "0") == "0" and \
+            os.environ.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
+        import tempfile
+        os.environ["NCCL_DEBUG"] = "INFO"
+        os.environ["NCCL_DEBUG_SUBSYS"] = "INIT"
+        os.environ["NCCL_DEBUG_FILE"] = os.path.join(tempfile.gettempdir(),
+                                                     f"optfuse_bench_nccl_{os.getpid()}.log")
+        NCCL_LOG = os.environ["NCCL_DEBUG_FILE"]
+NCCL_LOG = globals().get("NCCL_LOG")
+
 METRIC = "train iter time & images/sec (fused vs unfused) at 1/2/4/8 B200; update HBM GB/s"
 UNIT = "images/s"
 
@@ -122,11 +141,6 @@ class Dist:
         import torch.distributed as dist
         if self.world > 1 or force:
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            # communicator lines (ranks, transport, NVLS) for the driver's checks, on
-            # stderr so that the result stays the last stdout line
-            os.environ.setdefault("NCCL_DEBUG", "INFO")
-            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
             if backend == "nccl":
                 torch.cuda.set_device(self.local)
             dist.init_process_group(backend, rank=self.rank, world_size=self.world)
@@ -1156,6 +1170,9 @@ def main(argv=None):
         res = run_reference(args)
     else:
         res = run_ours(args)
+    if NCCL_LOG and os.path.exists(NCCL_LOG):   # rank 0's communicator lines, before the result
+        with open(NCCL_LOG) as fh:
+            sys.stdout.write(fh.read())
     if res is not None and int(os.environ.get("RANK", "0")) == 0:
         line = json.dumps(res, separators=(",", ":"))
         if len(line) > 2048:
