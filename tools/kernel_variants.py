@@ -19,8 +19,6 @@ if len(sys.argv) > 1 and sys.argv[1] == "--one":
 
 for so in sorted((ROOT / "build" / "variants").glob("*.so")):
     env = dict(os.environ, OPTFUSE_B200_LIB=str(so))
-    if "_tma" in so.name:
-        env["OPTFUSE_TMA"] = "1"
     out = subprocess.run([sys.executable, __file__, "--one"], env=env, capture_output=True, text=True)
     line = out.stdout.strip().splitlines()[-1] if out.stdout.strip() else out.stderr[-300:]
     print(so.name, line, flush=True)
