@@ -17,7 +17,8 @@ import bench  # noqa: E402
 def main():
     torch.backends.cudnn.benchmark = True
     torch.backends.cudnn.benchmark_limit = 0
-    torch.backends.cuda.matmul.allow_tf32 = True
+    torch.backends.cuda.matmul.allow_tf32 = False   # true fp32, as bench.py
+    torch.backends.cudnn.allow_tf32 = False
     dev = torch.device("cuda", 0)
     args = bench.parse_args([])
     args.world, args.dp = 1, False
