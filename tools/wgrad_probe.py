@@ -2,7 +2,7 @@
 (fixed cost + cost per 64-token block) for one shape, and a single launch
 for ncu.
 
-    python tools/wgrad_probe.py sweep [M N]     # JSON: tokens -> us (CUDA events, 20 back-to-back launches)
+    python tools/wgrad_probe.py sweep [M N]     # JSON: tokens -> us (CUDA events over 20 graph-captured launches)
     python tools/wgrad_probe.py one [M N T]     # one launch (for ncu -k regex:wgrad)
 """
 
@@ -36,26 +36,14 @@ def main():
         torch.cuda.synchronize()
         return
     M, N = (int(a) for a in sys.argv[2:4]) if len(sys.argv) > 3 else (3072, 768)
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    from wgrad_variants import graph_us   # 20 launches captured and replayed: device time only
     out = {"M": M, "N": N, "rows": []}
     for T in (256, 512, 1024, 2048, 4096, 8192):
         dy, x, th, m, v, hp = problem(M, N, T)
-        for _ in range(3):
-            kernels.wgrad_step(dy, x, th, m, v, hp)
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        a.record()
-        for _ in range(20):
-            kernels.wgrad_step(dy, x, th, m, v, hp)
-        b.record()
-        torch.cuda.synchronize()
-        us = a.elapsed_time(b) * 1e3 / 20
+        us = graph_us(lambda: kernels.wgrad_step(dy, x, th, m, v, hp))
         g = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-        a.record()
-        for _ in range(20):
-            torch.matmul(dy.t(), x, out=g)
-        b.record()
-        torch.cuda.synchronize()
-        cu = a.elapsed_time(b) * 1e3 / 20
+        cu = graph_us(lambda: torch.matmul(dy.t(), x, out=g))
         out["rows"].append({"T": T, "fused_us": round(us, 2), "cublas_us": round(cu, 2),
                             "fused_tflops": round(2 * M * N * T / us / 1e6, 1)})
     print(json.dumps(out))
