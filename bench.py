@@ -808,6 +808,11 @@ def run_ours(args) -> dict:
     arms = headline_arms(args)
     if args.headline_only:
         arms = arms[:1]
+    elif args.graphs and not args.dp:
+        # the same fused / unfused pair eager (no CUDA graph): the host issues
+        # every kernel there, and fusion hides its updates in the host's gaps
+        arms += [("eager:" + n, dict(kw, graphed=False)) for n, kw in arms
+                 if n in (arms[0][0], "ours:baseline", "torch.optim.SGD(foreach)")]
     times = {name: [] for name, _ in arms}
     head = arms[0][0]
     launches = 0
@@ -873,6 +878,13 @@ def run_ours(args) -> dict:
                        "speedup_vs_torch_fused": ratio(tp + "torch.optim.SGD(fused)"),
                        "torch_arm": unfused_torch + "torch.optim, same mode"},
            "gpu_launches": int(launches)}
+    if "eager:" + head in med:
+        eh = med["eager:" + head]
+        res["unfused"]["eager"] = {
+            "fused_ms": round(eh, 4), "ours_baseline_ms": med_ms("eager:ours:baseline"),
+            "torch_foreach_ms": med_ms("eager:torch.optim.SGD(foreach)"),
+            "speedup_vs_ours_unfused": round(med["eager:ours:baseline"] / eh, 4),
+            "speedup_vs_torch_foreach": round(med["eager:torch.optim.SGD(foreach)"] / eh, 4)}
     extras = {"rows": {k: {"ms_per_step": round(med[k], 4),
                            "images_per_s": round(dist.world * args.batch * 1e3 / med[k], 1),
                            "instances_ms": [round(t, 4) for t in v]} for k, v in times.items()},
