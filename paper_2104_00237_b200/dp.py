@@ -188,6 +188,8 @@ class DataParallelFusion:
         if self.mixed:
             for p in graph.parameters:
                 p.master = None
+        # single-device engines hold the parameters' old storage: drop them
+        graph._engines.clear()
         self.bucket_of = {p.id: b for b in self.buckets for p in b.params}
         self.scale = None
         if self.cuda:

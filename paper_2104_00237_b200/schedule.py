@@ -164,6 +164,9 @@ class _TraceRecorder:
                     self.steps_for_group(gi)
 
 
+_ALL_IN_ONE = 1 << 62   # bucket size that merges every layer into one launch group
+
+
 def _engine(graph: Graph, policy: OptimizerPolicy, side: bool, bucket_elems: int = 0,
             priority: str = "high", exclude=frozenset()):
     from .engine import FusionEngine
@@ -230,7 +233,20 @@ def run_baseline(graph: Graph, policy: OptimizerPolicy, inp, *, timing: bool = T
         if tc is not None:
             prev = tc.add_task(tr.CLIP_BARRIER, -1, (prev,))
     order = list(reversed(graph.parameters))
-    policy.step_params(order, trace=tc)
+    if tc is None and policy.clip_norm is None and graph.device.type == "cuda":
+        # the same single multi-tensor launch, its tensor list kept by the
+        # native engine (one group: every parameter, backward order): no
+        # per-parameter Python on the host, which an eager step pays for
+        policy.check_steppable(order)
+        eng = _engine(graph, policy, False, _ALL_IN_ONE)
+        eng.configure(policy, policy.t, None, 0)
+        eng.native.launch_group(0, sync=False)
+        eng.native.join()
+        for p in order:
+            p.pending = False
+            p._grad_scale = None
+    else:
+        policy.step_params(order, trace=tc)
     if tc is not None:
         for p in order:
             prev = tc.add_task(tr.OPT_STEP, p.id, (prev,))
